@@ -1,0 +1,171 @@
+/*
+ * orbitflow_b200.h - C ABI of the B200 (sm_100a) per-decode-step KV data path.
+ *
+ * This is the drop-in boundary underneath the kvsim host API
+ * (/root/reference/pkg/src/kvsim).  The reference only *prices* a decode step;
+ * every entry point below *does* the corresponding work on the GPU.  Each
+ * declaration cites the reference interface whose semantics it realises.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; no torch types.  Device pointers are
+ *     CUDA device (or UVA-mapped host) addresses, `stream` is a cudaStream_t
+ *     passed as void* (NULL = legacy default stream).
+ *   - Every function returns 0 on success, a cudaError_t value (>0) for a CUDA
+ *     failure, or -1 for an argument error; ofb_last_error() returns the
+ *     thread-local message.  There is no CPU fallback: a missing GPU is an
+ *     error (reference error convention: ValueError / RuntimeError classes,
+ *     kvsim/latency.py:78-79, kvsim/engine.py:53-58).
+ *   - KV layout (pool blocks, staging slots and host slabs alike): one paged
+ *     block of 16 tokens (kvsim DEFAULT_BLOCK_SIZE, core.py:24) for all KV heads
+ *     of one layer is  bf16 [Hkv][2 (K,V)][16][128]  = Hkv * 8 KiB.
+ *     A (request, layer) slab is a run of such blocks; in host memory it is
+ *     contiguous, in HBM it is addressed through a block table.
+ *   - head_dim must be 128; q-group Hq/Hkv must be <= 16.
+ */
+#ifndef ORBITFLOW_B200_H_
+#define ORBITFLOW_B200_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define OFB_API __attribute__((visibility("default")))
+#else
+#define OFB_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- library ----------------------------------------------------------- */
+OFB_API const char* ofb_version(void);
+OFB_API const char* ofb_last_error(void);
+/* SM count and resident attention CTAs per SM on the current device. */
+OFB_API int ofb_device_info(int32_t* num_sms, int32_t* attn_ctas_per_sm);
+
+/* ---- pinned host pool -------------------------------------------------- */
+/* Page-locked, device-mapped host memory (cudaHostAlloc Mapped|Portable).
+ * Backs the host-resident KV slabs: offloaded layers (x[r][l] = 0,
+ * kvsim/core.py:110-122) and evicted/removable layers (kvsim/engine.py:126-204).
+ * Returns NULL on failure. */
+OFB_API void* ofb_host_alloc(int64_t bytes);
+OFB_API int ofb_host_free(void* ptr);
+
+/* ---- K1: paged GQA flash-decode attention (one layer) ------------------ */
+/* Bytes of scratch ofb_decode_attention needs; zero it once before first use
+ * (the kernel re-arms its counters itself). */
+OFB_API int64_t ofb_attention_workspace_bytes(int32_t batch, int32_t num_q_heads,
+                                      int32_t num_kv_heads, int32_t max_seq_len);
+
+/* out[b][hq][:] = softmax(scale * q[b][hq] . K_b^T) V_b over the first
+ * seq_lens[b] tokens of request b's paged KV, with K/V of kv head hq/(Hq/Hkv).
+ * Realises the compute the reference prices as per_layer_compute
+ * (kvsim/core.py:257-261) inside batch_decode_latency_fast
+ * (kvsim/latency.py:252-274).
+ *   q, out        bf16 [batch][Hq][128]
+ *   kv_pool       block pool base, pool_blocks blocks of Hkv*8 KiB
+ *   block_tables  int32 [batch][max_blocks] pool block ids
+ *   seq_lens      int32 [batch] tokens per request (device)
+ *   max_seq_len   host-side upper bound of seq_lens (grid sizing) */
+OFB_API int ofb_decode_attention(const void* q, void* out, const void* kv_pool, int64_t pool_blocks,
+                         const int32_t* block_tables, int32_t max_blocks,
+                         const int32_t* seq_lens, void* workspace, int64_t workspace_bytes,
+                         int32_t batch, int32_t num_q_heads, int32_t num_kv_heads,
+                         int32_t head_dim, int32_t max_seq_len, float scale, void* stream);
+
+/* ---- K3: new-token KV append ------------------------------------------- */
+/* For every layer l < num_layers, request b, kv head h: write k_new/v_new
+ * [l][b][h][:] at token positions[b] (skip if < 0) into
+ *   - the pool block block_tables[l][b][positions[b]/16] (skip if < 0), and
+ *   - the mapped host slab host_slabs[l][b] (skip if 0 or host_slabs NULL).
+ * Realises RequestState.record_generated_token / sync_blocks
+ * (kvsim/core.py:95-102) as called per step at kvsim/engine.py:389-392, and
+ * the paper's "fresh KV written to its host slot" for offloaded layers
+ * (PAPER.md:489). */
+OFB_API int ofb_kv_append(const void* k_new, const void* v_new, void* kv_pool,
+                  const int32_t* block_tables, int32_t max_blocks, const int32_t* positions,
+                  const uint64_t* host_slabs, int32_t num_layers, int32_t batch,
+                  int32_t num_kv_heads, int32_t head_dim, void* stream);
+
+/* ---- K2 + K3 + K1: one decode step of the whole layer stack ------------ */
+typedef struct ofb_runtime ofb_runtime;
+
+typedef struct ofb_step_desc {
+  int32_t num_layers, batch, num_q_heads, num_kv_heads, head_dim;
+  float scale;
+  /* device tensors */
+  const void* q;              /* bf16 [L][B][Hq][128] */
+  void* out;                  /* bf16 [L][B][Hq][128] */
+  const void* k_new;          /* bf16 [L][B][Hkv][128] */
+  const void* v_new;          /* bf16 [L][B][Hkv][128] */
+  void* kv_pool;
+  int64_t pool_blocks;
+  const int32_t* block_tables; /* int32 [L][B][max_blocks]: resident slab or staging slot */
+  int32_t max_blocks;
+  const int32_t* seq_lens;    /* int32 [B], after this step's append */
+  const int32_t* positions;   /* int32 [B], index of the appended token (<0: no append) */
+  const uint64_t* host_slabs_dev; /* [L][B] mapped host slab bases, 0 = GPU-resident */
+  void* workspace;
+  int64_t workspace_bytes;
+  int32_t max_seq_len;
+  /* host-side transfer plan */
+  const uint64_t* host_slabs;  /* [L][B] same values, host copy: x[r][l]=0 <=> != 0 */
+  const uint64_t* staging_dst; /* [L][B] device address of the staging slot for (l, b) */
+  const int64_t* fetch_bytes;  /* [B] bytes fetched per offloaded (b, l) slab */
+  int32_t staging_slots;       /* 1 = reference single-slot launch rule, 2 = double buffer */
+  int32_t record_timing;       /* 1 = record per-layer / per-copy CUDA events */
+} ofb_step_desc;
+
+typedef struct ofb_step_timing {
+  int32_t layers;           /* attention launches timed */
+  float attn_ms_total;      /* sum of per-layer attention kernel durations */
+  float attn_ms_max;
+  int32_t copies;           /* H2D slab fetches timed */
+  float copy_ms_sum;        /* sum of per-copy durations */
+  double copy_bytes;        /* bytes fetched */
+  float copy_span_ms;       /* first copy start -> last copy end */
+  float step_ms;            /* step start -> last attention end */
+  int32_t copy_streams;     /* copy streams used */
+  float mig_ms;             /* last ofb_runtime_migrate span (0 if none timed) */
+  double mig_h2d_bytes, mig_d2h_bytes;
+} ofb_step_timing;
+
+OFB_API ofb_runtime* ofb_runtime_create(int32_t max_copy_streams);
+OFB_API int ofb_runtime_destroy(ofb_runtime* rt);
+
+/* Enqueue one full decode step on `stream` (the compute stream) plus the
+ * runtime's copy streams, asynchronously:
+ *   1. append (K3) for every layer (resident -> pool, offloaded -> host slab),
+ *   2. per request, one copy stream fetches its offloaded slabs in layer order
+ *      into its staging slot(s) (K2), honouring the reference launch rule
+ *      (kvsim/latency.py:159-169): with staging_slots = 1 the
+ *      fetch of offloaded layer l' starts only after the attention of that
+ *      request's previous offloaded layer released the slot,
+ *   3. per layer, attention (K1) waits only for the fetches whose destination
+ *      is that layer - the stall of kvsim/latency.py:185-187, now physical.
+ * Replaces the pricing call batch_decode_latency_fast at
+ * kvsim/engine.py:715-734 with the execution it prices. */
+OFB_API int ofb_runtime_decode_step(ofb_runtime* rt, const ofb_step_desc* desc, void* stream);
+
+/* K4: plan-change reconfiguration.  Enqueue n whole-slab moves
+ * (kind 0 = host->device restore, 1 = device->host eviction, 2 = device->device)
+ * on the migration streams after all work already on `stream`; `stream` (and
+ * the next decode step's copy streams) then wait for them.  Realises
+ * apply_plan (kvsim/engine.py:213-248), BlockTable.evict_for_space
+ * (kvsim/engine.py:184-204) and reconfiguration_delta (kvsim/latency.py:277-297). */
+OFB_API int ofb_runtime_migrate(ofb_runtime* rt, int32_t n, const uint64_t* dst, const uint64_t* src,
+                        const int64_t* bytes, const int32_t* kinds, int32_t record_timing,
+                        void* stream);
+
+/* Timing of the last decode step / migration (synchronises on their events). */
+OFB_API int ofb_runtime_timing(ofb_runtime* rt, ofb_step_timing* out);
+
+/* Host-link probe: best-of-reps pinned cudaMemcpyAsync in each direction. */
+OFB_API int ofb_link_probe(void* host, void* dev, int64_t bytes, int32_t reps, double* h2d_gbs,
+                   double* d2h_gbs);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ORBITFLOW_B200_H_ */

@@ -1,0 +1,119 @@
+"""ctypes binding of the sm_100a C ABI (``include/orbitflow_b200.h``).
+
+The library is the only compute path: if it is missing or fails to load the
+ops raise; nothing falls back to a CPU implementation.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+_LOCK = threading.Lock()
+_LIB = None
+
+c_i32 = ctypes.c_int32
+c_i64 = ctypes.c_int64
+c_f32 = ctypes.c_float
+c_f64 = ctypes.c_double
+c_vp = ctypes.c_void_p
+c_u64p = ctypes.POINTER(ctypes.c_uint64)
+c_i64p = ctypes.POINTER(ctypes.c_int64)
+c_i32p = ctypes.POINTER(ctypes.c_int32)
+
+
+class StepDesc(ctypes.Structure):
+    """Mirror of ``ofb_step_desc``."""
+
+    _fields_ = [
+        ("num_layers", c_i32), ("batch", c_i32), ("num_q_heads", c_i32),
+        ("num_kv_heads", c_i32), ("head_dim", c_i32),
+        ("scale", c_f32),
+        ("q", c_vp), ("out", c_vp), ("k_new", c_vp), ("v_new", c_vp),
+        ("kv_pool", c_vp), ("pool_blocks", c_i64),
+        ("block_tables", c_vp), ("max_blocks", c_i32),
+        ("seq_lens", c_vp), ("positions", c_vp), ("host_slabs_dev", c_vp),
+        ("workspace", c_vp), ("workspace_bytes", c_i64),
+        ("max_seq_len", c_i32),
+        ("host_slabs", c_vp), ("staging_dst", c_vp), ("fetch_bytes", c_vp),
+        ("staging_slots", c_i32), ("record_timing", c_i32),
+    ]
+
+
+class StepTiming(ctypes.Structure):
+    """Mirror of ``ofb_step_timing``."""
+
+    _fields_ = [
+        ("layers", c_i32), ("attn_ms_total", c_f32), ("attn_ms_max", c_f32),
+        ("copies", c_i32), ("copy_ms_sum", c_f32), ("copy_bytes", c_f64),
+        ("copy_span_ms", c_f32), ("step_ms", c_f32), ("copy_streams", c_i32),
+        ("mig_ms", c_f32), ("mig_h2d_bytes", c_f64), ("mig_d2h_bytes", c_f64),
+    ]
+
+
+# name -> (restype, argtypes); exactly the symbols include/orbitflow_b200.h declares
+SIGNATURES = {
+    "ofb_version": (ctypes.c_char_p, []),
+    "ofb_last_error": (ctypes.c_char_p, []),
+    "ofb_device_info": (ctypes.c_int, [c_i32p, c_i32p]),
+    "ofb_host_alloc": (c_vp, [c_i64]),
+    "ofb_host_free": (ctypes.c_int, [c_vp]),
+    "ofb_attention_workspace_bytes": (c_i64, [c_i32, c_i32, c_i32, c_i32]),
+    "ofb_decode_attention": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_i32, c_vp, c_vp, c_i64,
+                                            c_i32, c_i32, c_i32, c_i32, c_i32, c_f32, c_vp]),
+    "ofb_kv_append": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_i32,
+                                     c_i32, c_vp]),
+    "ofb_runtime_create": (c_vp, [c_i32]),
+    "ofb_runtime_destroy": (ctypes.c_int, [c_vp]),
+    "ofb_runtime_decode_step": (ctypes.c_int, [c_vp, ctypes.POINTER(StepDesc), c_vp]),
+    "ofb_runtime_migrate": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp]),
+    "ofb_runtime_timing": (ctypes.c_int, [c_vp, ctypes.POINTER(StepTiming)]),
+    "ofb_link_probe": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, ctypes.POINTER(c_f64),
+                                      ctypes.POINTER(c_f64)]),
+}
+
+
+class NativeError(RuntimeError):
+    """A call into the sm_100a library failed (CUDA error or bad argument)."""
+
+
+def lib_path() -> Path:
+    env = os.environ.get("OFB_LIB")
+    if env:
+        return Path(env)
+    return Path(__file__).resolve().parent / "_lib" / "liborbitflow_b200.so"
+
+
+def load(build_if_missing: bool = True):
+    """Load (building first if needed) the library; raises if unavailable."""
+    global _LIB
+    with _LOCK:
+        if _LIB is not None:
+            return _LIB
+        path = lib_path()
+        if not path.exists() and build_if_missing:
+            from . import build as _build
+
+            _build.build()
+        if not path.exists():
+            raise NativeError(f"sm_100a library not found at {path}; run __graft_entry__.build()")
+        # make sure torch's CUDA runtime is the one resolved first
+        try:
+            import torch  # noqa: F401
+        except Exception:  # pragma: no cover - torch is always present here
+            pass
+        lib = ctypes.CDLL(str(path), mode=ctypes.RTLD_GLOBAL)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _LIB = lib
+        return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = _LIB.ofb_last_error().decode() if _LIB is not None else ""
+        raise NativeError(f"{what} failed (rc={rc}): {msg}")

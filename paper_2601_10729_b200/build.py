@@ -1,0 +1,93 @@
+"""Build recipe for the sm_100a data-path library (``liborbitflow_b200.so``).
+
+Plain nvcc, in-tree output (``paper_2601_10729_b200/_lib``) so the built
+library travels with the repo snapshot to the GPU box.  No torch extension
+machinery: the library exposes the C ABI declared in
+``include/orbitflow_b200.h`` and is bound with ctypes (``_native.py``).
+"""
+
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+OUT_DIR = PKG / "_lib"
+LIB_NAME = "liborbitflow_b200.so"
+SOURCES = ["decode_attention.cu", "kv_append.cu", "runtime.cu"]
+
+ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = [
+    "-O3",
+    "-std=c++17",
+    "-lineinfo",
+    "-Xcompiler", "-fPIC",
+    "-Xcompiler", "-fvisibility=hidden",
+    "--expt-relaxed-constexpr",
+    "-cudart", "shared",
+]
+
+
+def nvcc() -> str:
+    cand = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    if not Path(cand).exists():
+        raise RuntimeError("nvcc not found: the sm_100a library cannot be built")
+    return cand
+
+
+def lib_path() -> Path:
+    return OUT_DIR / LIB_NAME
+
+
+def _stale(target: Path, deps) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(Path(d).stat().st_mtime > t for d in deps)
+
+
+def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = False) -> Path:
+    """Compile every .cu into one shared library; returns its path."""
+    OUT_DIR.mkdir(exist_ok=True)
+    target = lib_path()
+    deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "orbitflow_b200.h"]
+    if not force and not _stale(target, deps):
+        return target
+    objs = []
+    for src in SOURCES:
+        obj = OUT_DIR / (Path(src).stem + ".o")
+        cmd = [nvcc(), *ARCH_FLAGS, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(CSRC / src), "-o", str(obj)]
+        cmd.extend(["-Xcompiler", "-fvisibility=hidden"])
+        if ptxas_verbose:
+            cmd.extend(["-Xptxas", "-v"])
+        _run(cmd, verbose or ptxas_verbose)
+        objs.append(str(obj))
+    tmp = target.with_suffix(".so.tmp")
+    _run([nvcc(), *ARCH_FLAGS, "-shared", "-cudart", "shared", "-o", str(tmp), *objs, "-lcuda"
+          if _has_libcuda() else "-L/usr/local/cuda/lib64/stubs"], verbose)
+    os.replace(tmp, target)
+    return target
+
+
+def _has_libcuda() -> bool:
+    return False  # the driver entry point is resolved at run time (cudaGetDriverEntryPoint)
+
+
+def _run(cmd, verbose):
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if verbose and res.stderr:
+        print(res.stderr, file=sys.stderr)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+
+
+if __name__ == "__main__":
+    p = build(verbose="-v" in sys.argv, force="-f" in sys.argv, ptxas_verbose="--ptxas" in sys.argv)
+    print(p)

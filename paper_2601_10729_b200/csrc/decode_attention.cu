@@ -1,0 +1,446 @@
+// K1: paged GQA flash-decoding attention for one layer of a decode step.
+//
+// Realises what the reference only prices: per_layer_compute
+// (/root/reference/pkg/src/kvsim/core.py:257-261) is the stand-in cost of this
+// kernel; the paper's arithmetic is GQA decode over
+// 16-token paged blocks in a per-request, layer-aware table
+// (PAPER.md:750).
+//
+// Work decomposition: one CTA per (split, kv head, request).  A split is a
+// contiguous run of `blocks_per_split` paged blocks of that request's table.
+//   * warp 4 (producer): one elected lane streams the split's (block, head)
+//     K+V tiles (8 KiB each) into an 8-stage shared-memory ring with TMA
+//     (cp.async.bulk.tensor, 128B swizzle -> conflict-free ldmatrix).
+//   * warps 0-3 (consumers): warp w takes ring entries w, w+4, ...; each does
+//     S = Q.K^T and O += P.V for 16 tokens as mma.m16n8k16 tiles (the GQA
+//     group, <=16 query heads, is the M dimension; tokens / head dims are N),
+//     with an online softmax in registers (quad shuffles for row max).
+//   * the 4 warp states merge through shared memory; multi-split requests
+//     write (O, lse) partials and the last CTA of a (request, kv head) to
+//     arrive (atomic ticket) combines them - no second launch.
+#include "common.cuh"
+
+namespace ofb {
+
+constexpr int kConsumerWarps = 4;
+constexpr int kAttnThreads = (kConsumerWarps + 1) * 32;
+constexpr int kStages = 8;
+constexpr int kMaxSplits = 256;
+constexpr int kMaxBlocksPerSplit = 256;
+constexpr int kMaxGroup = 16;
+
+struct AttnArgs {
+  const __nv_bfloat16* q;       // [B][Hq][128]
+  __nv_bfloat16* out;           // [B][Hq][128]
+  const int32_t* block_tables;  // [B][max_blocks]
+  const int32_t* seq_lens;      // [B]
+  float* ws_o;                  // [B][Hq][max_splits][128]
+  float* ws_lse;                // [B][Hq][max_splits]   (log2 domain)
+  int32_t* counters;            // [B][Hkv], zero at rest
+  int max_blocks;
+  int hq, hkv, group;
+  int blocks_per_split, max_splits;
+  float scale_log2;
+};
+
+struct MergeScratch {
+  float o[kConsumerWarps][kMaxGroup][kHeadDim + 4];
+  float m[kConsumerWarps][kMaxGroup];
+  float l[kConsumerWarps][kMaxGroup];
+};
+
+constexpr size_t kRingBytes = size_t(kStages) * kHeadBlockBytes;
+static_assert(sizeof(MergeScratch) <= kRingBytes, "merge scratch must fit in the ring");
+static_assert(kMaxGroup * kMaxSplits * sizeof(float) + kMaxGroup * 2 * sizeof(float) <= kRingBytes,
+              "combine scratch must fit in the ring");
+
+constexpr size_t kAttnSmemBytes = 1024 /*align slack*/ + kRingBytes +
+                                  2 * kStages * sizeof(uint64_t) +
+                                  kMaxBlocksPerSplit * sizeof(int32_t) + 16;
+
+__device__ __forceinline__ uint32_t tile_addr(uint32_t base, int row, int chunk) {
+  // Tile = two 128B-swizzled halves of [32 rows][64 bf16]; `chunk` is the 16 B
+  // column unit (0..15) of the logical 256 B row.
+  return base + ((chunk >> 3) << 12) + (row << 7) + ((((chunk & 7) ^ (row & 7))) << 4);
+}
+
+__global__ void __launch_bounds__(kAttnThreads, 2)
+paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnArgs a) {
+  const int split = blockIdx.x;
+  const int kvh = blockIdx.y;
+  const int req = blockIdx.z;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+
+  const int seq = a.seq_lens[req];
+  const int nblk = (seq + kBlockTokens - 1) / kBlockTokens;
+  const int nsplit = (nblk + a.blocks_per_split - 1) / a.blocks_per_split;
+  const int g = a.group;
+  const int qh0 = kvh * g;
+
+  if (nblk == 0) {  // empty request: defined output
+    if (split == 0) {
+      for (int i = tid; i < g * kHeadDim; i += kAttnThreads)
+        a.out[((size_t)req * a.hq + qh0) * kHeadDim + i] = __float2bfloat16(0.f);
+    }
+    return;
+  }
+  if (split >= nsplit) return;
+  const int b_begin = split * a.blocks_per_split;
+  const int n = min(a.blocks_per_split, nblk - b_begin);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kRingBytes);
+  uint64_t* empty = full + kStages;
+  int32_t* blk_ids = reinterpret_cast<int32_t*>(empty + kStages);
+  int* flag = blk_ids + kMaxBlocksPerSplit;
+
+  const int32_t* bt = a.block_tables + (size_t)req * a.max_blocks + b_begin;
+  for (int i = tid; i < n; i += kAttnThreads) blk_ids[i] = bt[i];
+  if (tid == 0) {
+    prefetch_tma_desc(&kv_map);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const float NEG_INF = -INFINITY;
+  // per-lane softmax state (rows r0 and r0+8 of the padded 16-row group)
+  float o[16][4];
+  float m_run[2] = {NEG_INF, NEG_INF};
+  float l_run[2] = {0.f, 0.f};
+  const int r0 = lane >> 2;
+  const int c0 = (lane & 3) * 2;
+
+  if (warp == kConsumerWarps) {
+    // ---------------------------------------------------------- producer
+    if (lane == 0) {
+      for (int i = 0; i < n; ++i) {
+        const int st = i % kStages;
+        if (i >= kStages) mbar_wait(&empty[st], ((i / kStages) - 1) & 1);
+        const int row = (blk_ids[i] * a.hkv + kvh) * kTileRows;
+        uint8_t* dst = ring + (size_t)st * kHeadBlockBytes;
+        mbar_arrive_expect_tx(&full[st], kHeadBlockBytes);
+        tma_load_2d(dst, &kv_map, &full[st], 0, row);
+        tma_load_2d(dst + kHeadBlockBytes / 2, &kv_map, &full[st], 64, row);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- consumers
+    // Q as the A operand (rows = query heads of this group, zero padded).
+    uint32_t qa[8][4];
+    {
+      const __nv_bfloat16* qb = a.q + ((size_t)req * a.hq + qh0) * kHeadDim;
+      const bool v0 = r0 < g, v1 = (r0 + 8) < g;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const int col = kk * 16 + c0;
+        qa[kk][0] = v0 ? *reinterpret_cast<const uint32_t*>(qb + r0 * kHeadDim + col) : 0u;
+        qa[kk][1] = v1 ? *reinterpret_cast<const uint32_t*>(qb + (r0 + 8) * kHeadDim + col) : 0u;
+        qa[kk][2] = v0 ? *reinterpret_cast<const uint32_t*>(qb + r0 * kHeadDim + col + 8) : 0u;
+        qa[kk][3] = v1 ? *reinterpret_cast<const uint32_t*>(qb + (r0 + 8) * kHeadDim + col + 8) : 0u;
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
+
+    const int mi = lane >> 3;  // ldmatrix sub-matrix this lane addresses
+    const int mr = lane & 7;
+    for (int i = warp; i < n; i += kConsumerWarps) {
+      const int st = i % kStages;
+      mbar_wait(&full[st], (i / kStages) & 1);
+      const uint32_t base = smem_u32(ring + (size_t)st * kHeadBlockBytes);
+
+      // S = Q K^T over 16 tokens: s[j] covers tokens 8j..8j+7.
+      float s[2][4];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+#pragma unroll
+        for (int kp = 0; kp < 4; ++kp) {
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(tile_addr(base, j * 8 + mr, kp * 4 + mi), b0, b1, b2, b3);
+          mma_bf16_16816(s[j], qa[2 * kp], b0, b1);
+          mma_bf16_16816(s[j], qa[2 * kp + 1], b2, b3);
+        }
+      }
+      const int tok0 = (b_begin + i) * kBlockTokens;
+      const bool partial = tok0 + kBlockTokens > seq;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float v = s[j][e] * a.scale_log2;
+          if (partial && (tok0 + j * 8 + c0 + (e & 1)) >= seq) v = NEG_INF;
+          s[j][e] = v;
+        }
+      }
+      float mx0 = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
+      float mx1 = fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      const float mn0 = fmaxf(m_run[0], mx0);
+      const float mn1 = fmaxf(m_run[1], mx1);
+      const float corr0 = fast_exp2(m_run[0] - mn0);
+      const float corr1 = fast_exp2(m_run[1] - mn1);
+      m_run[0] = mn0;
+      m_run[1] = mn1;
+      float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        s[j][0] = fast_exp2(s[j][0] - mn0);
+        s[j][1] = fast_exp2(s[j][1] - mn0);
+        s[j][2] = fast_exp2(s[j][2] - mn1);
+        s[j][3] = fast_exp2(s[j][3] - mn1);
+        rs0 += s[j][0] + s[j][1];
+        rs1 += s[j][2] + s[j][3];
+      }
+      l_run[0] = l_run[0] * corr0 + rs0;
+      l_run[1] = l_run[1] * corr1 + rs1;
+#pragma unroll
+      for (int nt = 0; nt < 16; ++nt) {
+        o[nt][0] *= corr0;
+        o[nt][1] *= corr0;
+        o[nt][2] *= corr1;
+        o[nt][3] *= corr1;
+      }
+      // P (accumulator layout == A-operand layout for k16)
+      uint32_t pa[4];
+      pa[0] = pack_bf16(s[0][0], s[0][1]);
+      pa[1] = pack_bf16(s[0][2], s[0][3]);
+      pa[2] = pack_bf16(s[1][0], s[1][1]);
+      pa[3] = pack_bf16(s[1][2], s[1][3]);
+      // O += P V : V rows live at tile rows 16..31.
+#pragma unroll
+      for (int np = 0; np < 8; ++np) {
+        uint32_t v0, v1, v2, v3;
+        ldsm_x4_t(tile_addr(base, 16 + (mi & 1) * 8 + mr, 2 * np + (mi >> 1)), v0, v1, v2, v3);
+        mma_bf16_16816(o[2 * np], pa, v0, v1);
+        mma_bf16_16816(o[2 * np + 1], pa, v2, v3);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    l_run[0] += __shfl_xor_sync(0xffffffffu, l_run[0], 1);
+    l_run[0] += __shfl_xor_sync(0xffffffffu, l_run[0], 2);
+    l_run[1] += __shfl_xor_sync(0xffffffffu, l_run[1], 1);
+    l_run[1] += __shfl_xor_sync(0xffffffffu, l_run[1], 2);
+  }
+  __syncthreads();  // ring drained: every issued TMA was consumed
+
+  // -------------------------------------------------------- merge 4 warps
+  MergeScratch* ms = reinterpret_cast<MergeScratch*>(ring);
+  if (warp < kConsumerWarps) {
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) {
+      const int d = nt * 8 + c0;
+      ms->o[warp][r0][d] = o[nt][0];
+      ms->o[warp][r0][d + 1] = o[nt][1];
+      ms->o[warp][r0 + 8][d] = o[nt][2];
+      ms->o[warp][r0 + 8][d + 1] = o[nt][3];
+    }
+    if ((lane & 3) == 0) {
+      ms->m[warp][r0] = m_run[0];
+      ms->l[warp][r0] = l_run[0];
+      ms->m[warp][r0 + 8] = m_run[1];
+      ms->l[warp][r0 + 8] = l_run[1];
+    }
+  }
+  __syncthreads();
+
+  const bool single = (nsplit == 1);
+  for (int idx = tid; idx < g * kHeadDim; idx += kAttnThreads) {
+    const int row = idx / kHeadDim;
+    const int d = idx - row * kHeadDim;
+    float M = NEG_INF;
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, ms->m[w][row]);
+    float acc = 0.f, L = 0.f;
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w) {
+      const float mw = ms->m[w][row];
+      if (mw != NEG_INF) {
+        const float sc = fast_exp2(mw - M);
+        acc += sc * ms->o[w][row][d];
+        L += sc * ms->l[w][row];
+      }
+    }
+    const float val = acc / L;
+    const size_t qrow = (size_t)req * a.hq + qh0 + row;
+    if (single) {
+      a.out[qrow * kHeadDim + d] = __float2bfloat16(val);
+    } else {
+      a.ws_o[(qrow * a.max_splits + split) * kHeadDim + d] = val;
+      if (d == 0) a.ws_lse[qrow * a.max_splits + split] = M + __log2f(L);
+    }
+  }
+  if (single) return;
+
+  // ------------------------------------------- last CTA combines the splits
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const int ticket = atomicAdd(&a.counters[req * a.hkv + kvh], 1);
+    *flag = (ticket == nsplit - 1);
+  }
+  __syncthreads();
+  if (!*flag) return;
+  __threadfence();
+
+  float* wts = reinterpret_cast<float*>(ring);        // [16][nsplit]
+  float* inv = wts + kMaxGroup * kMaxSplits;          // [16]
+  for (int row = warp; row < g; row += kAttnThreads / 32) {
+    const size_t qrow = (size_t)req * a.hq + qh0 + row;
+    float M = NEG_INF;
+    for (int s2 = lane; s2 < nsplit; s2 += 32) {
+      const float v = __ldcg(&a.ws_lse[qrow * a.max_splits + s2]);
+      wts[row * kMaxSplits + s2] = v;
+      M = fmaxf(M, v);
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+    float S = 0.f;
+    for (int s2 = lane; s2 < nsplit; s2 += 32) {
+      const float w = fast_exp2(wts[row * kMaxSplits + s2] - M);
+      wts[row * kMaxSplits + s2] = w;
+      S += w;
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
+    if (lane == 0) inv[row] = 1.f / S;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < g * kHeadDim; idx += kAttnThreads) {
+    const int row = idx / kHeadDim;
+    const int d = idx - row * kHeadDim;
+    const size_t qrow = (size_t)req * a.hq + qh0 + row;
+    const float* src = a.ws_o + qrow * a.max_splits * kHeadDim + d;
+    float acc = 0.f;
+    for (int s2 = 0; s2 < nsplit; ++s2) acc += wts[row * kMaxSplits + s2] * __ldcg(src + (size_t)s2 * kHeadDim);
+    a.out[qrow * kHeadDim + d] = __float2bfloat16(acc * inv[row]);
+  }
+  if (tid == 0) a.counters[req * a.hkv + kvh] = 0;  // re-arm for the next launch
+}
+
+// ------------------------------------------------------------------ host side
+
+int encode_kv_map(CUtensorMap* map, void* pool, int64_t pool_blocks, int hkv);  // runtime.cu
+
+struct AttnPlan {
+  int blocks_per_split;
+  int max_splits;
+};
+
+static int g_attn_occupancy = 0;
+static int g_num_sms = 0;
+
+static cudaError_t attn_init_once() {
+  if (g_attn_occupancy > 0) return cudaSuccess;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(paged_gqa_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)kAttnSmemBytes);
+  if (e != cudaSuccess) return e;
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, paged_gqa_decode_kernel, kAttnThreads,
+                                                    kAttnSmemBytes);
+  if (e != cudaSuccess) return e;
+  g_attn_occupancy = occ > 0 ? occ : 1;
+  return cudaSuccess;
+}
+
+// Pick the split length that minimises (waves x split length) for the widest
+// request: grids are sized against 148 SMs x resident CTAs per SM.
+static AttnPlan plan_splits(int batch, int hkv, int max_seq_len) {
+  const int nblk = (max_seq_len + kBlockTokens - 1) / kBlockTokens;
+  AttnPlan p{1, 1};
+  if (nblk <= 0) return p;
+  const long slots = (long)g_num_sms * g_attn_occupancy;
+  const long pairs = (long)batch * hkv;
+  int lo = (nblk + kMaxSplits - 1) / kMaxSplits;
+  lo = lo < 1 ? 1 : lo;
+  int hi = nblk < kMaxBlocksPerSplit ? nblk : kMaxBlocksPerSplit;
+  if (lo > hi) lo = hi;
+  double best = 1e300;
+  for (int bps = lo; bps <= hi; ++bps) {
+    const long splits = (nblk + bps - 1) / bps;
+    const long ctas = pairs * splits;
+    const long waves = (ctas + slots - 1) / slots;
+    // per-CTA fixed cost ~ 3 blocks of streaming (pipeline fill + merge),
+    // plus the combine pass reading `splits` partials when split.
+    const double cost = (double)waves * (bps + 3.0) + (splits > 1 ? 0.05 * splits : 0.0);
+    if (cost < best - 1e-9) {
+      best = cost;
+      p.blocks_per_split = bps;
+    }
+  }
+  p.max_splits = (nblk + p.blocks_per_split - 1) / p.blocks_per_split;
+  return p;
+}
+
+size_t attention_workspace_bytes(int batch, int hq, int hkv, int max_seq_len) {
+  const int nblk = (max_seq_len + kBlockTokens - 1) / kBlockTokens;
+  int splits = nblk < 1 ? 1 : nblk;
+  if (splits > kMaxSplits) splits = kMaxSplits;
+  const size_t counters = ((size_t)batch * hkv * sizeof(int32_t) + 255) & ~size_t(255);
+  const size_t lse = ((size_t)batch * hq * splits * sizeof(float) + 255) & ~size_t(255);
+  const size_t o = (size_t)batch * hq * splits * kHeadDim * sizeof(float);
+  return counters + lse + o;
+}
+
+cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void* out,
+                                    const int32_t* block_tables, int max_blocks,
+                                    const int32_t* seq_lens, void* workspace,
+                                    size_t workspace_bytes, int batch, int hq, int hkv,
+                                    int max_seq_len, float scale, cudaStream_t stream) {
+  if (batch <= 0) return cudaSuccess;
+  if (hkv <= 0 || hq % hkv != 0 || hq / hkv > kMaxGroup) return cudaErrorInvalidValue;
+  cudaError_t e = attn_init_once();
+  if (e != cudaSuccess) return e;
+  if (workspace_bytes < attention_workspace_bytes(batch, hq, hkv, max_seq_len))
+    return cudaErrorInvalidValue;
+  const AttnPlan plan = plan_splits(batch, hkv, max_seq_len);
+  const int nblk = (max_seq_len + kBlockTokens - 1) / kBlockTokens;
+  int ws_splits = nblk < 1 ? 1 : nblk;
+  if (ws_splits > kMaxSplits) ws_splits = kMaxSplits;
+
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  const size_t counters = ((size_t)batch * hkv * sizeof(int32_t) + 255) & ~size_t(255);
+  const size_t lse = ((size_t)batch * hq * ws_splits * sizeof(float) + 255) & ~size_t(255);
+
+  AttnArgs a;
+  a.q = static_cast<const __nv_bfloat16*>(q);
+  a.out = static_cast<__nv_bfloat16*>(out);
+  a.block_tables = block_tables;
+  a.seq_lens = seq_lens;
+  a.counters = reinterpret_cast<int32_t*>(ws);
+  a.ws_lse = reinterpret_cast<float*>(ws + counters);
+  a.ws_o = reinterpret_cast<float*>(ws + counters + lse);
+  a.max_blocks = max_blocks;
+  a.hq = hq;
+  a.hkv = hkv;
+  a.group = hq / hkv;
+  a.blocks_per_split = plan.blocks_per_split;
+  a.max_splits = ws_splits;
+  a.scale_log2 = scale * 1.4426950408889634f;
+  dim3 grid(plan.max_splits, hkv, batch);
+  paged_gqa_decode_kernel<<<grid, kAttnThreads, kAttnSmemBytes, stream>>>(map, a);
+  return cudaGetLastError();
+}
+
+int attention_occupancy() {
+  attn_init_once();
+  return g_attn_occupancy;
+}
+
+}  // namespace ofb

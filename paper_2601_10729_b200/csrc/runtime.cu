@@ -1,0 +1,553 @@
+// Native step runtime + C ABI (include/orbitflow_b200.h).
+//
+// K2 (offloaded-layer streaming) and K4 (plan-change migration) live here as
+// copy-engine work ordered by CUDA events; K1/K3 launches are issued on the
+// caller's compute stream.  One ofb_runtime_decode_step call enqueues a whole
+// step (1 append + L attention launches + every slab fetch) without blocking
+// the host, so the reference's Alg.-1 schedule (kvsim/latency.py:141-209) is
+// enforced by the GPU itself rather than simulated.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/orbitflow_b200.h"
+#include "common.cuh"
+
+namespace ofb {
+size_t attention_workspace_bytes(int batch, int hq, int hkv, int max_seq_len);
+cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void* out,
+                                    const int32_t* block_tables, int max_blocks,
+                                    const int32_t* seq_lens, void* workspace,
+                                    size_t workspace_bytes, int batch, int hq, int hkv,
+                                    int max_seq_len, float scale, cudaStream_t stream);
+cudaError_t launch_kv_append(const void* k_new, const void* v_new, void* pool,
+                             const int32_t* block_tables, int max_blocks,
+                             const int32_t* positions, const uint64_t* host_slabs,
+                             int num_layers, int batch, int hkv, bool device_write_with_host,
+                             cudaStream_t stream);
+int attention_occupancy();
+}  // namespace ofb
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code == 0 ? -1 : code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return static_cast<int>(e);
+}
+
+#define OFB_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);  \
+  } while (0)
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+int load_encoder() {
+  if (g_encode) return 0;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  OFB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (q != cudaDriverEntryPointSuccess || fn == nullptr)
+    return fail(-1, "cuTensorMapEncodeTiled not available from the driver");
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return 0;
+}
+
+// Tensor-map cache: the pool is described as a 2-D bf16 tensor of 128-wide
+// rows (one token row of one head, K or V); one box = 32 rows (K tile + V tile
+// of one (block, head)) x 64 columns, 128-byte swizzled.
+struct MapCache {
+  std::mutex mu;
+  struct Entry {
+    void* pool;
+    int64_t blocks;
+    int hkv;
+    alignas(64) CUtensorMap map;
+  };
+  std::vector<Entry> entries;
+};
+MapCache g_maps;
+
+int get_kv_map(void* pool, int64_t pool_blocks, int hkv, CUtensorMap* out) {
+  std::lock_guard<std::mutex> lock(g_maps.mu);
+  for (auto& e : g_maps.entries) {
+    if (e.pool == pool && e.blocks == pool_blocks && e.hkv == hkv) {
+      *out = e.map;
+      return 0;
+    }
+  }
+  int rc = load_encoder();
+  if (rc) return rc;
+  MapCache::Entry e;
+  e.pool = pool;
+  e.blocks = pool_blocks;
+  e.hkv = hkv;
+  const uint64_t rows = static_cast<uint64_t>(pool_blocks) * hkv * ofb::kTileRows;
+  if (rows >= (1ull << 32)) return fail(-1, "kv pool too large for one tensor map");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(ofb::kHeadDim), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ofb::kRowBytes)};
+  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(ofb::kTileRows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(&e.map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, pool, dims, strides, box,
+                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(-1, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  if (g_maps.entries.size() > 64) g_maps.entries.erase(g_maps.entries.begin());
+  g_maps.entries.push_back(e);
+  *out = e.map;
+  return 0;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ runtime
+
+struct CopyTiming {
+  cudaEvent_t start, stop;
+  double bytes;
+  int stream;
+};
+
+struct ofb_runtime {
+  int device = 0;
+  int max_streams = 16;
+  std::vector<cudaStream_t> copy;
+  cudaStream_t mig_h2d = nullptr, mig_d2h = nullptr;
+  std::vector<cudaEvent_t> sync_events;  // timing-disabled, reused every step
+  size_t next_sync = 0;
+  std::vector<cudaEvent_t> timing_events;
+  size_t next_timing = 0;
+  // last-step timing records
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> attn_t;
+  std::vector<CopyTiming> copy_t;
+  cudaEvent_t step_start = nullptr;
+  bool timed = false;
+  int streams_used = 0;
+  // migration
+  bool pending_mig = false;
+  cudaEvent_t mig_done_h2d = nullptr, mig_done_d2h = nullptr;
+  cudaEvent_t mig_t0 = nullptr, mig_t1 = nullptr, mig_t2 = nullptr;
+  bool mig_timed = false;
+  double mig_h2d_bytes = 0, mig_d2h_bytes = 0;
+  std::vector<int> order_buf;
+};
+
+namespace {
+
+int next_sync_event(ofb_runtime* rt, cudaEvent_t* ev) {
+  if (rt->next_sync == rt->sync_events.size()) {
+    cudaEvent_t e;
+    OFB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    rt->sync_events.push_back(e);
+  }
+  *ev = rt->sync_events[rt->next_sync++];
+  return 0;
+}
+
+int next_timing_event(ofb_runtime* rt, cudaEvent_t* ev) {
+  if (rt->next_timing == rt->timing_events.size()) {
+    cudaEvent_t e;
+    OFB_CUDA(cudaEventCreate(&e));
+    rt->timing_events.push_back(e);
+  }
+  *ev = rt->timing_events[rt->next_timing++];
+  return 0;
+}
+
+int ensure_streams(ofb_runtime* rt, int n) {
+  while (static_cast<int>(rt->copy.size()) < n) {
+    cudaStream_t s;
+    OFB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    rt->copy.push_back(s);
+  }
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ofb_version(void) { return "orbitflow-b200 0.1 sm_100a"; }
+
+const char* ofb_last_error(void) { return g_err.c_str(); }
+
+int ofb_device_info(int32_t* num_sms, int32_t* attn_ctas_per_sm) {
+  int dev = 0;
+  OFB_CUDA(cudaGetDevice(&dev));
+  int sms = 0;
+  OFB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (num_sms) *num_sms = sms;
+  if (attn_ctas_per_sm) *attn_ctas_per_sm = ofb::attention_occupancy();
+  return 0;
+}
+
+void* ofb_host_alloc(int64_t bytes) {
+  if (bytes <= 0) {
+    g_err = "ofb_host_alloc: bytes must be > 0";
+    return nullptr;
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaHostAlloc(&p, static_cast<size_t>(bytes),
+                                cudaHostAllocMapped | cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    cuda_fail(e, "cudaHostAlloc");
+    return nullptr;
+  }
+  return p;
+}
+
+int ofb_host_free(void* ptr) {
+  if (ptr) OFB_CUDA(cudaFreeHost(ptr));
+  return 0;
+}
+
+int64_t ofb_attention_workspace_bytes(int32_t batch, int32_t num_q_heads, int32_t num_kv_heads,
+                                      int32_t max_seq_len) {
+  return static_cast<int64_t>(
+      ofb::attention_workspace_bytes(batch, num_q_heads, num_kv_heads, max_seq_len));
+}
+
+static int check_shapes(int32_t batch, int32_t hq, int32_t hkv, int32_t head_dim) {
+  if (head_dim != ofb::kHeadDim) return fail(-1, "head_dim must be 128");
+  if (batch < 0 || hq <= 0 || hkv <= 0) return fail(-1, "batch/heads must be positive");
+  if (hq % hkv != 0 || hq / hkv > 16) return fail(-1, "Hq must be a multiple of Hkv with group <= 16");
+  return 0;
+}
+
+int ofb_decode_attention(const void* q, void* out, const void* kv_pool, int64_t pool_blocks,
+                         const int32_t* block_tables, int32_t max_blocks,
+                         const int32_t* seq_lens, void* workspace, int64_t workspace_bytes,
+                         int32_t batch, int32_t num_q_heads, int32_t num_kv_heads,
+                         int32_t head_dim, int32_t max_seq_len, float scale, void* stream) {
+  int rc = check_shapes(batch, num_q_heads, num_kv_heads, head_dim);
+  if (rc) return rc;
+  if (batch == 0) return 0;
+  if (!q || !out || !kv_pool || !block_tables || !seq_lens || !workspace)
+    return fail(-1, "ofb_decode_attention: null pointer");
+  if (max_seq_len > max_blocks * ofb::kBlockTokens)
+    return fail(-1, "max_seq_len exceeds the block-table width");
+  CUtensorMap map;
+  rc = get_kv_map(const_cast<void*>(kv_pool), pool_blocks, num_kv_heads, &map);
+  if (rc) return rc;
+  cudaError_t e = ofb::launch_decode_attention(
+      map, q, out, block_tables, max_blocks, seq_lens, workspace,
+      static_cast<size_t>(workspace_bytes), batch, num_q_heads, num_kv_heads, max_seq_len, scale,
+      static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "paged_gqa_decode_kernel launch");
+  return 0;
+}
+
+int ofb_kv_append(const void* k_new, const void* v_new, void* kv_pool,
+                  const int32_t* block_tables, int32_t max_blocks, const int32_t* positions,
+                  const uint64_t* host_slabs, int32_t num_layers, int32_t batch,
+                  int32_t num_kv_heads, int32_t head_dim, void* stream) {
+  if (head_dim != ofb::kHeadDim) return fail(-1, "head_dim must be 128");
+  if (num_kv_heads <= 0 || num_kv_heads * 32 > 1024 * 64) return fail(-1, "bad num_kv_heads");
+  if (!k_new || !v_new || !positions) return fail(-1, "ofb_kv_append: null pointer");
+  if (block_tables && !kv_pool) return fail(-1, "ofb_kv_append: block tables need a pool");
+  cudaError_t e = ofb::launch_kv_append(k_new, v_new, kv_pool, block_tables, max_blocks,
+                                        positions, host_slabs, num_layers, batch, num_kv_heads,
+                                        true, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "kv_append_kernel launch");
+  return 0;
+}
+
+ofb_runtime* ofb_runtime_create(int32_t max_copy_streams) {
+  ofb_runtime* rt = new ofb_runtime();
+  if (cudaGetDevice(&rt->device) != cudaSuccess) {
+    g_err = "ofb_runtime_create: no CUDA device";
+    delete rt;
+    return nullptr;
+  }
+  rt->max_streams = std::max(1, std::min<int>(max_copy_streams, 64));
+  bool ok = cudaStreamCreateWithFlags(&rt->mig_h2d, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&rt->mig_d2h, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&rt->mig_done_h2d, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&rt->mig_done_d2h, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreate(&rt->mig_t0) == cudaSuccess &&
+            cudaEventCreate(&rt->mig_t1) == cudaSuccess &&
+            cudaEventCreate(&rt->mig_t2) == cudaSuccess;
+  if (!ok) {
+    g_err = "ofb_runtime_create: stream/event creation failed";
+    delete rt;
+    return nullptr;
+  }
+  return rt;
+}
+
+int ofb_runtime_destroy(ofb_runtime* rt) {
+  if (!rt) return 0;
+  cudaDeviceSynchronize();
+  for (auto s : rt->copy) cudaStreamDestroy(s);
+  if (rt->mig_h2d) cudaStreamDestroy(rt->mig_h2d);
+  if (rt->mig_d2h) cudaStreamDestroy(rt->mig_d2h);
+  for (auto e : rt->sync_events) cudaEventDestroy(e);
+  for (auto e : rt->timing_events) cudaEventDestroy(e);
+  for (cudaEvent_t e : {rt->mig_done_h2d, rt->mig_done_d2h, rt->mig_t0, rt->mig_t1, rt->mig_t2})
+    if (e) cudaEventDestroy(e);
+  delete rt;
+  return 0;
+}
+
+int ofb_runtime_decode_step(ofb_runtime* rt, const ofb_step_desc* d, void* stream_) {
+  if (!rt || !d) return fail(-1, "ofb_runtime_decode_step: null argument");
+  int rc = check_shapes(d->batch, d->num_q_heads, d->num_kv_heads, d->head_dim);
+  if (rc) return rc;
+  const int L = d->num_layers, B = d->batch;
+  if (L <= 0) return fail(-1, "num_layers must be > 0");
+  if (B == 0) return 0;
+  if (d->staging_slots < 1 || d->staging_slots > 8) return fail(-1, "staging_slots must be 1..8");
+  if (!d->host_slabs || !d->staging_dst || !d->fetch_bytes)
+    return fail(-1, "host transfer plan arrays are required");
+  cudaStream_t cs = static_cast<cudaStream_t>(stream_);
+  CUtensorMap map;
+  rc = get_kv_map(d->kv_pool, d->pool_blocks, d->num_kv_heads, &map);
+  if (rc) return rc;
+
+  rt->next_sync = 0;
+  rt->next_timing = 0;
+  rt->attn_t.clear();
+  rt->copy_t.clear();
+  rt->timed = d->record_timing != 0;
+
+  // Per-request offload lists (layer order) -> this step's fetch schedule.
+  std::vector<std::vector<int>> offl(B);
+  bool any_fetch = false;
+  for (int l = 0; l < L; ++l)
+    for (int b = 0; b < B; ++b)
+      if (d->host_slabs[(size_t)l * B + b] != 0) {
+        offl[b].push_back(l);
+        any_fetch = true;
+      }
+  const int nstreams = any_fetch ? std::min(B, rt->max_streams) : 0;
+  rc = ensure_streams(rt, nstreams);
+  if (rc) return rc;
+  rt->streams_used = nstreams;
+
+  // Step start: a pending migration, then the append of every layer.  Copy
+  // streams start after it: staging from the previous step is released and
+  // host slabs already hold this step's token.
+  if (rt->pending_mig) {
+    OFB_CUDA(cudaStreamWaitEvent(cs, rt->mig_done_h2d, 0));
+    OFB_CUDA(cudaStreamWaitEvent(cs, rt->mig_done_d2h, 0));
+    rt->pending_mig = false;
+  }
+  if (rt->timed) {
+    rc = next_timing_event(rt, &rt->step_start);
+    if (rc) return rc;
+    OFB_CUDA(cudaEventRecord(rt->step_start, cs));
+  }
+  cudaError_t e = ofb::launch_kv_append(d->k_new, d->v_new, d->kv_pool, d->block_tables,
+                                        d->max_blocks, d->positions, d->host_slabs_dev, L, B,
+                                        d->num_kv_heads, false, cs);
+  if (e != cudaSuccess) return cuda_fail(e, "kv_append_kernel launch");
+  cudaEvent_t ev_start;
+  rc = next_sync_event(rt, &ev_start);
+  if (rc) return rc;
+  OFB_CUDA(cudaEventRecord(ev_start, cs));
+  for (int s = 0; s < nstreams; ++s) OFB_CUDA(cudaStreamWaitEvent(rt->copy[s], ev_start, 0));
+
+  std::vector<cudaEvent_t> attn_done(L, nullptr);
+  std::vector<cudaEvent_t> fetch_done((size_t)L * B, nullptr);
+  std::vector<size_t> next(B, 0);
+  const int S = d->staging_slots;
+  const size_t q_layer = (size_t)B * d->num_q_heads * ofb::kHeadDim * 2;
+  const size_t bt_layer = (size_t)B * d->max_blocks;
+
+  for (int l = 0; l < L; ++l) {
+    // Fetches whose staging slot is (or will be, in stream order) free.
+    for (int b = 0; b < B; ++b) {
+      while (next[b] < offl[b].size()) {
+        const size_t k = next[b];
+        const int dst_layer = offl[b][k];
+        cudaStream_t s = rt->copy[b % nstreams];
+        if (k >= (size_t)S) {
+          const int prev = offl[b][k - S];
+          if (prev >= l) break;  // that layer's attention is not enqueued yet
+          OFB_CUDA(cudaStreamWaitEvent(s, attn_done[prev], 0));
+        }
+        const size_t idx = (size_t)dst_layer * B + b;
+        cudaEvent_t t0 = nullptr, t1 = nullptr;
+        if (rt->timed) {
+          if ((rc = next_timing_event(rt, &t0)) || (rc = next_timing_event(rt, &t1))) return rc;
+          OFB_CUDA(cudaEventRecord(t0, s));
+        }
+        OFB_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(d->staging_dst[idx]),
+                                 reinterpret_cast<const void*>(d->host_slabs[idx]),
+                                 static_cast<size_t>(d->fetch_bytes[b]), cudaMemcpyHostToDevice, s));
+        if (rt->timed) {
+          OFB_CUDA(cudaEventRecord(t1, s));
+          rt->copy_t.push_back({t0, t1, static_cast<double>(d->fetch_bytes[b]), b % nstreams});
+        }
+        cudaEvent_t done;
+        if ((rc = next_sync_event(rt, &done))) return rc;
+        OFB_CUDA(cudaEventRecord(done, s));
+        fetch_done[idx] = done;
+        ++next[b];
+      }
+    }
+    // Layer l: stall until its own fetches landed (latency.py:185-187), then attend.
+    for (int b = 0; b < B; ++b) {
+      cudaEvent_t f = fetch_done[(size_t)l * B + b];
+      if (f) OFB_CUDA(cudaStreamWaitEvent(cs, f, 0));
+    }
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (rt->timed) {
+      if ((rc = next_timing_event(rt, &t0)) || (rc = next_timing_event(rt, &t1))) return rc;
+      OFB_CUDA(cudaEventRecord(t0, cs));
+    }
+    e = ofb::launch_decode_attention(
+        map, static_cast<const uint8_t*>(d->q) + l * q_layer,
+        static_cast<uint8_t*>(d->out) + l * q_layer, d->block_tables + l * bt_layer, d->max_blocks,
+        d->seq_lens, d->workspace, static_cast<size_t>(d->workspace_bytes), B, d->num_q_heads,
+        d->num_kv_heads, d->max_seq_len, d->scale, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "paged_gqa_decode_kernel launch");
+    if (rt->timed) {
+      OFB_CUDA(cudaEventRecord(t1, cs));
+      rt->attn_t.push_back({t0, t1});
+    }
+    if (any_fetch) {
+      cudaEvent_t done;
+      if ((rc = next_sync_event(rt, &done))) return rc;
+      OFB_CUDA(cudaEventRecord(done, cs));
+      attn_done[l] = done;
+    }
+  }
+  for (int b = 0; b < B; ++b)
+    if (next[b] != offl[b].size()) return fail(-1, "internal: fetch schedule did not drain");
+  return 0;
+}
+
+int ofb_runtime_migrate(ofb_runtime* rt, int32_t n, const uint64_t* dst, const uint64_t* src,
+                        const int64_t* bytes, const int32_t* kinds, int32_t record_timing,
+                        void* stream_) {
+  if (!rt) return fail(-1, "ofb_runtime_migrate: null runtime");
+  if (n <= 0) return 0;
+  if (!dst || !src || !bytes || !kinds) return fail(-1, "ofb_runtime_migrate: null array");
+  cudaStream_t cs = static_cast<cudaStream_t>(stream_);
+  cudaEvent_t ev;
+  rt->next_sync = 0;
+  int rc = next_sync_event(rt, &ev);
+  if (rc) return rc;
+  OFB_CUDA(cudaEventRecord(ev, cs));
+  OFB_CUDA(cudaStreamWaitEvent(rt->mig_h2d, ev, 0));
+  OFB_CUDA(cudaStreamWaitEvent(rt->mig_d2h, ev, 0));
+  rt->mig_timed = record_timing != 0;
+  if (rt->mig_timed) OFB_CUDA(cudaEventRecord(rt->mig_t0, cs));
+  rt->mig_h2d_bytes = rt->mig_d2h_bytes = 0;
+  for (int i = 0; i < n; ++i) {
+    cudaMemcpyKind kind;
+    cudaStream_t s;
+    switch (kinds[i]) {
+      case 0: kind = cudaMemcpyHostToDevice; s = rt->mig_h2d; rt->mig_h2d_bytes += bytes[i]; break;
+      case 1: kind = cudaMemcpyDeviceToHost; s = rt->mig_d2h; rt->mig_d2h_bytes += bytes[i]; break;
+      case 2: kind = cudaMemcpyDeviceToDevice; s = rt->mig_h2d; break;
+      default: return fail(-1, "ofb_runtime_migrate: bad kind");
+    }
+    if (bytes[i] <= 0) continue;
+    OFB_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(dst[i]), reinterpret_cast<const void*>(src[i]),
+                             static_cast<size_t>(bytes[i]), kind, s));
+  }
+  OFB_CUDA(cudaEventRecord(rt->mig_done_h2d, rt->mig_h2d));
+  OFB_CUDA(cudaEventRecord(rt->mig_done_d2h, rt->mig_d2h));
+  if (rt->mig_timed) {
+    OFB_CUDA(cudaEventRecord(rt->mig_t1, rt->mig_h2d));
+    OFB_CUDA(cudaEventRecord(rt->mig_t2, rt->mig_d2h));
+  }
+  // Later compute (and the next step's fetches, via its start event) waits.
+  OFB_CUDA(cudaStreamWaitEvent(cs, rt->mig_done_h2d, 0));
+  OFB_CUDA(cudaStreamWaitEvent(cs, rt->mig_done_d2h, 0));
+  rt->pending_mig = false;
+  return 0;
+}
+
+int ofb_runtime_timing(ofb_runtime* rt, ofb_step_timing* out) {
+  if (!rt || !out) return fail(-1, "ofb_runtime_timing: null argument");
+  std::memset(out, 0, sizeof(*out));
+  out->copy_streams = rt->streams_used;
+  if (rt->timed) {
+    float ms = 0;
+    for (auto& p : rt->attn_t) {
+      OFB_CUDA(cudaEventSynchronize(p.second));
+      OFB_CUDA(cudaEventElapsedTime(&ms, p.first, p.second));
+      out->attn_ms_total += ms;
+      out->attn_ms_max = std::max(out->attn_ms_max, ms);
+    }
+    out->layers = static_cast<int32_t>(rt->attn_t.size());
+    if (!rt->attn_t.empty()) {
+      OFB_CUDA(cudaEventElapsedTime(&ms, rt->step_start, rt->attn_t.back().second));
+      out->step_ms = ms;
+    }
+    float first = 1e30f, last = 0.f;
+    for (auto& c : rt->copy_t) {
+      OFB_CUDA(cudaEventSynchronize(c.stop));
+      OFB_CUDA(cudaEventElapsedTime(&ms, c.start, c.stop));
+      out->copy_ms_sum += ms;
+      out->copy_bytes += c.bytes;
+      float a = 0, b = 0;
+      OFB_CUDA(cudaEventElapsedTime(&a, rt->step_start, c.start));
+      OFB_CUDA(cudaEventElapsedTime(&b, rt->step_start, c.stop));
+      first = std::min(first, a);
+      last = std::max(last, b);
+    }
+    out->copies = static_cast<int32_t>(rt->copy_t.size());
+    out->copy_span_ms = rt->copy_t.empty() ? 0.f : last - first;
+  }
+  if (rt->mig_timed) {
+    float a = 0, b = 0;
+    OFB_CUDA(cudaEventSynchronize(rt->mig_t1));
+    OFB_CUDA(cudaEventSynchronize(rt->mig_t2));
+    OFB_CUDA(cudaEventElapsedTime(&a, rt->mig_t0, rt->mig_t1));
+    OFB_CUDA(cudaEventElapsedTime(&b, rt->mig_t0, rt->mig_t2));
+    out->mig_ms = std::max(a, b);
+    out->mig_h2d_bytes = rt->mig_h2d_bytes;
+    out->mig_d2h_bytes = rt->mig_d2h_bytes;
+  }
+  return 0;
+}
+
+int ofb_link_probe(void* host, void* dev, int64_t bytes, int32_t reps, double* h2d_gbs,
+                   double* d2h_gbs) {
+  if (!host || !dev || bytes <= 0 || reps <= 0) return fail(-1, "ofb_link_probe: bad arguments");
+  cudaStream_t s;
+  cudaEvent_t a, b;
+  OFB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  OFB_CUDA(cudaEventCreate(&a));
+  OFB_CUDA(cudaEventCreate(&b));
+  double best[2] = {0, 0};
+  for (int dir = 0; dir < 2; ++dir) {
+    for (int i = 0; i < reps; ++i) {
+      OFB_CUDA(cudaEventRecord(a, s));
+      if (dir == 0)
+        OFB_CUDA(cudaMemcpyAsync(dev, host, (size_t)bytes, cudaMemcpyHostToDevice, s));
+      else
+        OFB_CUDA(cudaMemcpyAsync(host, dev, (size_t)bytes, cudaMemcpyDeviceToHost, s));
+      OFB_CUDA(cudaEventRecord(b, s));
+      OFB_CUDA(cudaEventSynchronize(b));
+      float ms = 0;
+      OFB_CUDA(cudaEventElapsedTime(&ms, a, b));
+      best[dir] = std::max(best[dir], (double)bytes / (ms * 1e-3) / 1e9);
+    }
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaStreamDestroy(s);
+  if (h2d_gbs) *h2d_gbs = best[0];
+  if (d2h_gbs) *d2h_gbs = best[1];
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,125 @@
+"""K1 (paged GQA decode attention) and K3 (append) on the GPU vs the CPU oracle.
+
+Tolerance (BASELINE.json north_star): bf16 GPU output vs the fp32/f64 CPU
+oracle within 2e-2 relative / 1e-2 absolute.  The append is byte work and is
+checked bit-exactly.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from kvgen import BLOCK, D, bf16_bits, make_case
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 2e-2, 1e-2
+
+
+def _run_gpu(case, max_seq_len=None):
+    from paper_2601_10729_b200 import ops
+
+    dev = torch.device("cuda:0")
+    out = ops.decode_attention(
+        case["q"].to(dev), case["pool"].to(dev),
+        torch.from_numpy(case["block_tables"]).to(dev),
+        torch.from_numpy(case["seq_lens"]).to(dev),
+        max_seq_len=max_seq_len, scale=case["scale"])
+    torch.cuda.synchronize()
+    return out.float().cpu().numpy()
+
+
+def _run_oracle(case):
+    return oracle.decode_attention(bf16_bits(case["q"]), bf16_bits(case["pool"]),
+                                   case["block_tables"], case["seq_lens"], case["scale"])
+
+
+@pytest.mark.parametrize("seq_lens,hq,hkv", [
+    ([4088, 4088, 4088, 4088], 8, 2),          # cfg1 toy shape (group 4)
+    ([4089, 17, 1, 300], 8, 2),                  # ragged, partial last blocks
+    ([1000, 2048], 32, 8),                       # Llama-3.1-8B heads (group 4)
+    ([3000, 5], 64, 8),                          # Llama-3.1-70B heads (group 8)
+    ([777], 16, 1),                              # group 16 (max)
+    ([513, 64], 4, 4),                           # MHA (group 1)
+])
+def test_attention_matches_oracle(seq_lens, hq, hkv):
+    case = make_case(seq_lens, hq, hkv, seed=sum(seq_lens) + hq)
+    got = _run_gpu(case)
+    want = _run_oracle(case)
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+
+
+def test_long_context_many_splits_and_rearm():
+    # 40K tokens on one (request, head): dozens of splits, last-CTA combine;
+    # a second launch checks that the split counters re-armed themselves.
+    case = make_case([40000, 31], 4, 1, seed=7)
+    first = _run_gpu(case)
+    second = _run_gpu(case)
+    want = _run_oracle(case)
+    np.testing.assert_allclose(first, want, rtol=RTOL, atol=ATOL)
+    np.testing.assert_array_equal(first, second)
+
+
+def test_empty_request_gives_zeros():
+    case = make_case([0, 100], 8, 2, seed=3)
+    got = _run_gpu(case, max_seq_len=100)
+    assert np.all(got[0] == 0.0)
+    np.testing.assert_allclose(got[1], _run_oracle(case)[1], rtol=RTOL, atol=ATOL)
+
+
+def test_oracle_self_check_dense():
+    # the oracle itself vs an independent dense float64 softmax(QK^T)V
+    case = make_case([200], 8, 2, seed=11)
+    want = _run_oracle(case)
+    bt = case["block_tables"][0]
+    pool = case["pool"].float().numpy()
+    k = np.concatenate([pool[bt[i], :, 0] for i in range(13)], axis=1)[:, :200]  # [Hkv, T, D]
+    v = np.concatenate([pool[bt[i], :, 1] for i in range(13)], axis=1)[:, :200]
+    dense = oracle.dense_attention_f64(case["q"][0].float().numpy(), k.transpose(1, 0, 2),
+                                       v.transpose(1, 0, 2), case["scale"])
+    np.testing.assert_allclose(want[0], dense, rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("positions", [[4088, 17, 0, 300], [15, 16, 31, 47]])
+def test_append_bit_exact(positions):
+    from paper_2601_10729_b200 import ops
+
+    hkv, b = 2, len(positions)
+    case = make_case([p + 1 for p in positions], 8, hkv, seed=5)
+    g = torch.Generator().manual_seed(99)
+    k_new = torch.randn((b, hkv, D), generator=g).to(torch.bfloat16)
+    v_new = torch.randn((b, hkv, D), generator=g).to(torch.bfloat16)
+    pos = np.asarray(positions, dtype=np.int32)
+
+    want = bf16_bits(case["pool"]).copy()
+    oracle.kv_append(bf16_bits(k_new), bf16_bits(v_new), want, case["block_tables"], pos)
+
+    dev = torch.device("cuda:0")
+    pool = case["pool"].to(dev)
+    ops.kv_append(k_new.to(dev), v_new.to(dev), pool, torch.from_numpy(case["block_tables"]).to(dev),
+                  torch.from_numpy(pos).to(dev))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(bf16_bits(pool.cpu()), want)
+
+
+def test_append_then_attend_sees_new_token():
+    from paper_2601_10729_b200 import ops
+
+    case = make_case([4096, 34], 8, 2, seed=21)
+    g = torch.Generator().manual_seed(5)
+    k_new = torch.randn((2, 2, D), generator=g).to(torch.bfloat16)
+    v_new = torch.randn((2, 2, D), generator=g).to(torch.bfloat16)
+    pos = np.asarray([4095, 33], dtype=np.int32)  # slot 15 of block 255; slot 1 of block 2
+    dev = torch.device("cuda:0")
+    pool = case["pool"].to(dev)
+    bt = torch.from_numpy(case["block_tables"]).to(dev)
+    ops.kv_append(k_new.to(dev), v_new.to(dev), pool, bt, torch.from_numpy(pos).to(dev))
+    lens = torch.from_numpy(pos + 1).to(dev)
+    got = ops.decode_attention(case["q"].to(dev), pool, bt, lens, scale=case["scale"])
+    torch.cuda.synchronize()
+    host_pool = bf16_bits(case["pool"]).copy()
+    oracle.kv_append(bf16_bits(k_new), bf16_bits(v_new), host_pool, case["block_tables"], pos)
+    want = oracle.decode_attention(bf16_bits(case["q"]), host_pool, case["block_tables"], pos + 1,
+                                   case["scale"])
+    np.testing.assert_allclose(got.float().cpu().numpy(), want, rtol=RTOL, atol=ATOL)
