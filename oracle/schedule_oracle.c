@@ -10,7 +10,8 @@
  *     (:159-169), equal-share completion order by (remaining, dest, request)
  *     (:172-184), blocking max (:185-187), window progress with the
  *     1e-9*(1+window) completion slack (:36, :189-204);
- *     total = comp*L + sum(stalls) (latency.py:264-266).
+ *     total = comp*L + sum(stalls) (latency.py:264-266), with sum() being
+ *     CPython's compensated float sum (see pysum_t).
  *   - oracle_blocks_to_fetch      latency.py:99-105
  *   - oracle_prefetch_buffer      latency.py:108-119 (Eq. 1)
  *   - oracle_reconfiguration_delta latency.py:277-297
@@ -24,6 +25,36 @@
 #include <stdlib.h>
 
 #define SLACK_EPS 1e-9
+
+/* CPython >= 3.12 builtin sum() over floats: Neumaier-compensated running sum
+ * (Python/bltinmodule.c builtin_sum_impl).  sum(stalls) in the reference
+ * (latency.py:266, planner.py:192) therefore rounds differently from a plain
+ * left fold; restated here so totals match to the bit.  The first term enters
+ * exactly (0 + s1 == s1), compensation starts with the second. */
+typedef struct {
+  double f, c;
+  int started;
+} pysum_t;
+
+static void pysum_add(pysum_t* s, double x) {
+  if (!s->started) {
+    s->f = 0.0 + x;
+    s->started = 1;
+    return;
+  }
+  const double t = s->f + x;
+  if (fabs(s->f) >= fabs(x))
+    s->c += (s->f - t) + x;
+  else
+    s->c += (x - t) + s->f;
+  s->f = t;
+}
+
+static double pysum_result(const pysum_t* s) {
+  double f = s->started ? s->f : 0.0;
+  if (s->c != 0.0 && isfinite(s->c)) f += s->c;
+  return f;
+}
 
 typedef struct {
   int active;
@@ -39,7 +70,7 @@ double oracle_stall_schedule(int32_t n, const int64_t* sizes, const uint8_t* off
   stream_t* st = (stream_t*)calloc((size_t)(n > 0 ? n : 1), sizeof(stream_t));
   int* next = (int*)calloc((size_t)(n > 0 ? n : 1), sizeof(int));
   int* order = (int*)malloc(sizeof(int) * (size_t)(n > 0 ? n : 1));
-  double stall_sum = 0.0;
+  pysum_t stall_sum = {0.0, 0.0, 0};
   for (int layer = 1; layer <= L; ++layer) {
     /* launch rule at the boundary of `layer` */
     for (int r = 0; r < n; ++r) {
@@ -109,12 +140,12 @@ double oracle_stall_schedule(int32_t n, const int64_t* sizes, const uint8_t* off
       }
     }
     if (stalls_out) stalls_out[layer - 1] = stall;
-    stall_sum = stall_sum + stall;
+    pysum_add(&stall_sum, stall);
   }
   free(st);
   free(next);
   free(order);
-  return comp * (double)L + stall_sum;
+  return comp * (double)L + pysum_result(&stall_sum);
 }
 
 int64_t oracle_blocks_to_fetch(int32_t n, const int64_t* sizes, const uint8_t* offloaded, int32_t L) {

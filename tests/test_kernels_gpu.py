@@ -68,19 +68,6 @@ def test_empty_request_gives_zeros():
     np.testing.assert_allclose(got[1], _run_oracle(case)[1], rtol=RTOL, atol=ATOL)
 
 
-def test_oracle_self_check_dense():
-    # the oracle itself vs an independent dense float64 softmax(QK^T)V
-    case = make_case([200], 8, 2, seed=11)
-    want = _run_oracle(case)
-    bt = case["block_tables"][0]
-    pool = case["pool"].float().numpy()
-    k = np.concatenate([pool[bt[i], :, 0] for i in range(13)], axis=1)[:, :200]  # [Hkv, T, D]
-    v = np.concatenate([pool[bt[i], :, 1] for i in range(13)], axis=1)[:, :200]
-    dense = oracle.dense_attention_f64(case["q"][0].float().numpy(), k.transpose(1, 0, 2),
-                                       v.transpose(1, 0, 2), case["scale"])
-    np.testing.assert_allclose(want[0], dense, rtol=1e-5, atol=1e-6)
-
-
 @pytest.mark.parametrize("positions", [[4088, 17, 0, 300], [15, 16, 31, 47]])
 def test_append_bit_exact(positions):
     from paper_2601_10729_b200 import ops

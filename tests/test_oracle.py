@@ -1,0 +1,81 @@
+"""Pin the CPU oracle before trusting it (CPU-only).
+
+* schedule_oracle.c vs golden vectors produced by the reference's own
+  _simulate_stalls (tests/golden/schedule_vectors.json): bit-exact floats;
+* the reference's known-answer tests for the Fig.-3 instance
+  (/root/reference/pkg/tests/test_latency.py:38, :57, :61, :96, :100, :226);
+* attn_oracle.c vs an independent float64 dense softmax(QK^T)V (the
+  reference has no attention, so this part is "parity unpinned" by it).
+"""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import torch
+
+import oracle
+from kvgen import bf16_bits, make_case
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+def test_schedule_oracle_matches_reference_vectors():
+    cases = json.loads((GOLDEN / "schedule_vectors.json").read_text())
+    for c in cases:
+        total, stalls = oracle.stall_schedule(c["sizes"], c["offloaded"], float.fromhex(c["comp"]),
+                                              float.fromhex(c["bw"]))
+        assert [float(s).hex() for s in stalls] == c["stalls"]
+        assert float(total).hex() == c["total"]
+
+
+def _fig3(prompts, generated):
+    sizes = [-(-(p + generated) // 16) for p in prompts]
+    return sizes
+
+
+def test_fig3_known_answers():
+    # two requests, 9 layers, stride 3 (placement A), 1 ms/layer, 3 blocks/ms
+    off_a = [[1 if l % 3 == 0 else 0 for l in range(1, 10)] for _ in range(2)]
+    step1 = _fig3([34, 81], 0)    # b = (3, 6)
+    step16 = _fig3([34, 81], 15)  # b = (4, 6)
+    assert step1 == [3, 6] and step16 == [4, 6]
+    assert oracle.blocks_to_fetch(step1, off_a) == 27                 # test_latency.py:38
+    assert oracle.prefetch_buffer(step1, off_a) == 9                  # :57
+    off_c = [[1 if l % 4 == 0 else 0 for l in range(1, 10)],
+             [1 if l % 3 == 0 else 0 for l in range(1, 10)]]
+    assert oracle.prefetch_buffer(step16, off_c) == 6                 # :61
+    total1, _ = oracle.stall_schedule(step1, off_a, 1.0, 3.0)
+    total16, _ = oracle.stall_schedule(step16, off_a, 1.0, 3.0)
+    assert (total1 - 9.0) * 3.0 == 9.0                                # :96 stall units
+    assert (total16 - 9.0) * 3.0 == 12.0                              # :100
+    res_a = np.array(off_a) ^ 1
+    res_c = np.array(off_c) ^ 1
+    assert oracle.reconfiguration_delta(step16, res_a, res_c) == (12, 8)   # :226
+
+
+def test_attention_oracle_vs_dense_f64():
+    case = make_case([200, 37], 8, 2, seed=11)
+    got = oracle.decode_attention(bf16_bits(case["q"]), bf16_bits(case["pool"]),
+                                  case["block_tables"], case["seq_lens"], case["scale"], threads=2)
+    pool = case["pool"].float().numpy()
+    for b, seq in enumerate(case["seq_lens"]):
+        nblk = -(-int(seq) // 16)
+        bt = case["block_tables"][b][:nblk]
+        k = np.concatenate([pool[i, :, 0] for i in bt], axis=1)[:, :seq]
+        v = np.concatenate([pool[i, :, 1] for i in bt], axis=1)[:, :seq]
+        dense = oracle.dense_attention_f64(case["q"][b].float().numpy(), k.transpose(1, 0, 2),
+                                           v.transpose(1, 0, 2), case["scale"])
+        np.testing.assert_allclose(got[b], dense, rtol=1e-5, atol=1e-6)
+
+
+def test_append_oracle_writes_the_right_slot():
+    case = make_case([40], 8, 2, seed=2)
+    pool = bf16_bits(case["pool"]).copy()
+    g = torch.Generator().manual_seed(1)
+    k = bf16_bits(torch.randn((1, 2, 128), generator=g).to(torch.bfloat16))
+    v = bf16_bits(torch.randn((1, 2, 128), generator=g).to(torch.bfloat16))
+    oracle.kv_append(k, v, pool, case["block_tables"], np.array([39], dtype=np.int32))
+    blk = case["block_tables"][0][39 // 16]
+    assert np.array_equal(pool[blk, 1, 0, 39 % 16], k[0, 1])
+    assert np.array_equal(pool[blk, 0, 1, 39 % 16], v[0, 0])
