@@ -1,0 +1,403 @@
+"""Benchmark of the per-decode-step KV data path (BASELINE.json config 2).
+
+Workload (default ``--config cfg2``): Llama-3.1-8B attention shape (32 layers,
+32 q / 8 KV heads, d=128, bf16 KV), batch 16, prompts of 32760 tokens
+(mid-block), placement ``from_strides(..., [2]*16)``: layers
+2,4,..,32 of every request live in pinned host memory (50%), the rest in HBM.
+One step = K3 append + K2 fetch of every offloaded slab (32 GiB over PCIe)
++ K1 attention on all 32 layers, enqueued by one native runtime call.
+
+Prints one JSON line (rank 0).  ``value``: tokens/s with step inputs resident
+in HBM; ``e2e``: the same through the public API with q / k_new / v_new
+copied from pinned host memory and the attention output read back every
+step.  ``roofline``: K1 (the dominant kernel) vs measured HBM copy peak;
+``step_roofline``: the binding host link (north-star target >= 0.70).
+``--impl reference``: the reference has no GPU path and no attention at all
+(kvsim prices steps); its arm times the CPU restatement of the data path
+(oracle/, kind "port") on this host's cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "decode tokens/sec + TPOT SLO attainment; per-step attn+fetch GB/s vs HBM/PCIe roofline"
+PCIE5_NOMINAL_GBS = 63.0
+
+CONFIGS = {
+    # name: (layers, hq, hkv, batch, prompt, stride, output)
+    "cfg1": dict(layers=4, hq=8, hkv=2, batch=4, prompt=4088, strides=[1, 1, None, None],
+                 output=64, workload="toy 4-layer GQA (8q/2kv, d=128), B=4, 4K ctx, reference "
+                                     "solve plan: requests 0,1 fully host-resident"),
+    "cfg2": dict(layers=32, hq=32, hkv=8, batch=16, prompt=32760, strides=[2] * 16, output=64,
+                 workload="Llama-3.1-8B shape (32 layers, 32q/8kv, d=128, bf16), B=16, 32K ctx, "
+                          "stride-2 plan: 50% of layers' KV host-resident, 1xB200"),
+}
+
+
+def _env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
+        int(os.environ.get("LOCAL_RANK", 0))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def _measured_peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+def build_batch(cfg):
+    from paper_2601_10729_b200.core import PlacementMatrix, RequestState
+
+    batch = [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=cfg["prompt"],
+                          target_output_tokens=cfg["output"]) for i in range(cfg["batch"])]
+    placement = PlacementMatrix.from_strides([r.id for r in batch], cfg["layers"], cfg["strides"])
+    return batch, placement
+
+
+class CpuAttentionSample:
+    """The CPU restatement of K1 (oracle/attn_oracle.c, all host threads) over
+    host-resident KV of one layer per call: the cpu_baseline / reference arm."""
+
+    def __init__(self, shape, batch, arena=None, arena_tables=None):
+        import numpy as np
+
+        import oracle
+
+        self.oracle = oracle
+        self.threads = oracle.host_threads()
+        B = len(batch)
+        self.lens = np.array([r.total_tokens + 1 for r in batch], dtype=np.int32)
+        nblk = [-(-int(t) // 16) for t in self.lens]
+        rng = np.random.default_rng(0)
+        if arena is None:
+            total = sum(nblk)
+            vals = rng.standard_normal(size=total * shape.block_bytes // 2, dtype=np.float32)
+            self.pool = (vals.view(np.uint32) >> 16).astype(np.uint16).reshape(
+                total, shape.num_kv_heads, 2, 16, 128)
+            del vals
+            tables = np.full((B, max(nblk)), -1, dtype=np.int32)
+            cur = 0
+            for b, n in enumerate(nblk):
+                tables[b, :n] = np.arange(cur, cur + n)
+                cur += n
+            self.tables = [tables]
+        else:
+            self.pool = arena.view_u16(0, arena.blocks).reshape(
+                arena.blocks, shape.num_kv_heads, 2, 16, 128)
+            self.tables = arena_tables
+        self.q = (rng.standard_normal((B, shape.num_q_heads, 128), dtype=np.float32)
+                  .view(np.uint32) >> 16).astype(np.uint16)
+        self.scale = 1.0 / math.sqrt(128)
+
+    def run(self, seconds_target: float):
+        """Attend layer after layer until ~seconds_target; returns (s/layer, layers)."""
+        t0 = time.perf_counter()
+        done = 0
+        while True:
+            self.oracle.decode_attention(self.q, self.pool, self.tables[done % len(self.tables)],
+                                         self.lens, self.scale, threads=self.threads)
+            done += 1
+            el = time.perf_counter() - t0
+            if el >= seconds_target or done >= 64 or el / done * (done + 1) > seconds_target * 1.5:
+                return el / done, done
+
+
+def run_reference_arm(args, cfg):
+    """CPU restatement of the path (oracle port) on this host's cores."""
+    from paper_2601_10729_b200.executor import ModelShape
+
+    rank, world, _ = _env_rank()
+    if rank != 0:
+        return
+    shape = ModelShape(cfg["layers"], cfg["hq"], cfg["hkv"])
+    batch, _placement = build_batch(cfg)
+    per_layer = []
+    sampler = CpuAttentionSample(shape, batch)
+    threads = sampler.threads
+    for _ in range(args.warmup):
+        sampler.run(0.0)
+    samples = []
+    for _ in range(args.steps):
+        s, n = sampler.run(args.ref_seconds)
+        per_layer.append(s)
+        samples.append(n)
+    step_s = statistics.median(per_layer) * cfg["layers"]
+    value = cfg["batch"] / step_s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64-accum over bf16 KV", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "sample": "1 layer (all requests) per step, "
+                                                         "scaled x layers"},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
+                         "sample": f"{samples[0]} layer(s) of {cfg['batch']} requests x "
+                                   f"{cfg['prompt']} tokens per step, scaled to "
+                                   f"{cfg['layers']} layers; reference kvsim has no attention"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfg):
+    import numpy as np
+    import torch
+
+    from paper_2601_10729_b200 import ops
+    from paper_2601_10729_b200.executor import B200Executor, ModelShape
+    from paper_2601_10729_b200.latency import blocks_to_fetch
+    from paper_2601_10729_b200.runtime import link_probe
+
+    rank, world, local = _env_rank()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist  # noqa: F811
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    hkv_total, hq_total = cfg["hkv"], cfg["hq"]
+    if hkv_total % world:
+        raise SystemExit(f"KV heads ({hkv_total}) must divide by the GPU count ({world})")
+    # KV-head sharding: each rank owns Hkv/N KV heads + their q heads
+    shape = ModelShape(cfg["layers"], hq_total // world, hkv_total // world)
+    batch, placement = build_batch(cfg)
+    L, B = cfg["layers"], cfg["batch"]
+    cap = -(-(cfg["prompt"] + cfg["output"] + 1) // 16)
+    n_off = sum(row.count(0) for row in placement.rows)
+    n_res = L * B - n_off
+    slots = args.staging_slots
+    device_blocks = n_res * cap + B * slots * cap + 16
+    host_blocks = max(n_off * cap, 1) + 16
+    ex = B200Executor(shape, device=dev, device_blocks=device_blocks, host_blocks=host_blocks,
+                      staging_slots=slots, copy_streams=args.copy_streams, seed=rank,
+                      record_timing=True)
+    # host-link peaks on this GPU (1 GiB pinned, best of 10) - before the data lands
+    probe_bytes = min(1 << 30, ex.host.nbytes, ex.pool.tensor.numel() * 2)
+    h2d_peak, d2h_peak = link_probe(ex.host.base, ex.pool.base, probe_bytes, 10)
+    ex.install(batch, placement)
+    torch.cuda.synchronize()
+
+    inputs = [ex.synthetic_inputs(B, step=i) for i in range(2)]
+    pinned = [{k: v.cpu().pin_memory() for k, v in inp.items()} for inp in inputs]
+    out_host = torch.empty_like(inputs[0]["q"], device="cpu").pin_memory()
+
+    attn_tokens = []
+
+    def step(i, e2e=False):
+        attn_tokens.append(sum(r.total_tokens + 1 for r in batch))
+        if e2e:
+            dev_in = {k: v.to(dev, non_blocking=True) for k, v in pinned[i % 2].items()}
+            ms = ex.decode_step(batch, None, dev_in)
+            out_host.copy_(ex.last_output, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        else:
+            ms = ex.decode_step(batch, None, inputs[i % 2])
+        for r in batch:
+            r.record_generated_token()
+        return ms
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        step(i)
+    barrier()
+    attn_tokens.clear()
+    timings = []
+    steps_ms = []
+    with ClockSampler(local) as clocks:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record()
+        for i in range(args.steps):
+            steps_ms.append(step(i))
+            timings.append(dict(ex.last_timing))
+        t_end.record()
+        barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    if dist is not None:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+
+    # e2e through the public API with host buffers
+    barrier()
+    e0 = time.perf_counter()
+    e2e_steps = max(2, args.steps // 2)
+    for i in range(e2e_steps):
+        step(i, e2e=True)
+    barrier()
+    e2e_ms = (time.perf_counter() - e0) * 1e3 / e2e_steps
+    if dist is not None:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    h2d_in = sum(v.numel() * v.element_size() for v in pinned[0].values())
+    d2h_out = out_host.numel() * out_host.element_size()
+
+    # roofline of K1 (dominant kernel): algorithmic bytes per launch / event duration
+    peaks = _measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    attn_ms = sum(t["attn_ms_total"] for t in timings) / sum(t["layers"] for t in timings)
+    tokens_per_layer = sum(attn_tokens[: args.steps]) / args.steps
+    kv_bytes = tokens_per_layer * shape.kv_bytes_per_token
+    qo_bytes = 2 * B * shape.num_q_heads * 128 * 2
+    attn_bytes = kv_bytes + qo_bytes
+    attn_gbs = attn_bytes / (attn_ms * 1e-3) / 1e9
+
+    # step roofline: host link (HOST_alg) vs HBM (HBM_alg), SURVEY.md 8(d)
+    host_alg = timings[-1]["copy_bytes"]
+    hbm_alg = L * attn_bytes + B * L * shape.kv_bytes_per_token
+    roof_ms = max(hbm_alg / (hbm_peak * 1e9), host_alg / (h2d_peak * 1e9)) * 1e3
+    copy_span = statistics.median(t["copy_span_ms"] for t in timings)
+    bound = "host_link" if host_alg / h2d_peak > hbm_alg / hbm_peak else "hbm"
+
+    value = B / (ms_per_step * 1e-3)  # whole job: every rank serves the same B tokens (TP)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        off_layers = sorted({l for row in placement.rows for l, bit in enumerate(row) if bit == 0})
+        tables = []
+        for l in off_layers[:4]:
+            if any(ex.slabs[r.id].host[l] is None for r in batch):
+                continue
+            t = np.full((B, cap), -1, dtype=np.int32)
+            for b, r in enumerate(batch):
+                t[b] = ex.slabs[r.id].host[l] + np.arange(cap, dtype=np.int32)
+            tables.append(t)
+        sampler = CpuAttentionSample(shape, batch, arena=ex.host, arena_tables=tables) \
+            if tables else CpuAttentionSample(shape, batch)
+        per_layer_s, layers_done = sampler.run(args.ref_seconds)
+        cpu_step = per_layer_s * L
+        cpu = {"value": B / cpu_step, "unit": "tokens/s", "cores": sampler.threads, "kind": "port",
+               "sample": f"{layers_done} layer(s) x {B} requests x ~{cfg['prompt']} tokens of "
+                         f"host-resident KV through oracle/attn_oracle.c, scaled to {L} layers"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) KV, q)",
+        "config": {"workload": cfg["workload"], "global_batch": B, "seq_len": cfg["prompt"],
+                   "layers": L, "q_heads": hq_total, "kv_heads": hkv_total,
+                   "parallelism": f"tp{world} (KV-head sharded)" if world > 1 else "single GPU",
+                   "offloaded_slabs": n_off, "staging_slots": slots,
+                   "copy_streams": timings[-1]["copy_streams"],
+                   "l2": "inputs (64 GiB KV) larger than the 126 MB L2; no flush needed"},
+        "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": h2d_in, "d2h_bytes_per_step": d2h_out},
+        "roofline": {"bound": "hbm", "kernel": "paged_gqa_decode_kernel (K1)",
+                     "achieved": attn_gbs, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": attn_gbs / hbm_peak, "traffic": None,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
+                     "bytes_per_launch": attn_bytes, "launch_ms": attn_ms,
+                     "frac_of_8tbs_nominal": attn_gbs / 8000.0},
+        "step_roofline": {"bound": bound, "achieved_frac": roof_ms / ms_per_step,
+                          "roofline_ms": roof_ms, "measured_ms": ms_per_step,
+                          "host_alg_bytes": host_alg, "hbm_alg_bytes": hbm_alg,
+                          "h2d_peak_gbs": h2d_peak, "d2h_peak_gbs": d2h_peak,
+                          "host_link_gbs": host_alg / (ms_per_step * 1e-3) / 1e9,
+                          "copy_span_ms": copy_span,
+                          "copy_gbs_during_span": host_alg / (copy_span * 1e-3) / 1e9,
+                          "frac_of_pcie5_nominal": host_alg / (ms_per_step * 1e-3) / 1e9
+                          / PCIE5_NOMINAL_GBS,
+                          "blocks_to_fetch_check": blocks_to_fetch(placement, batch)},
+        "gpu_launches": args.steps * (1 + L + len({l for row in placement.rows
+                                                   for l, b in enumerate(row) if b == 0})),
+        "clocks": clocks.summary(),
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ex.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
+    ap.add_argument("--staging-slots", type=int, default=1)
+    ap.add_argument("--copy-streams", type=int, default=16)
+    ap.add_argument("--ref-seconds", type=float, default=3.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -28,6 +28,10 @@ constexpr int kStages = 8;
 constexpr int kMaxSplits = 256;
 constexpr int kMaxBlocksPerSplit = 256;
 constexpr int kMaxGroup = 16;
+// Split tickets live in a fixed region at the start of the workspace, sized for
+// the largest (request x kv head) grid, so partials of a previous launch with
+// a different batch can never alias a counter.
+constexpr size_t kCounterRegionBytes = 65536;      // 16384 (request, kv head) pairs
 
 struct AttnArgs {
   const __nv_bfloat16* q;       // [B][Hq][128]
@@ -155,6 +159,21 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
       const int st = i % kStages;
       mbar_wait(&full[st], (i / kStages) & 1);
       const uint32_t base = smem_u32(ring + (size_t)st * kHeadBlockBytes);
+      const int tok0 = (b_begin + i) * kBlockTokens;
+      const bool partial = tok0 + kBlockTokens > seq;
+      if (partial) {
+        // Slots past the sequence end hold whatever the block held before
+        // (possibly NaN bit patterns): P is 0 there, but 0 * NaN poisons the
+        // P.V tile, so clear those V rows (tile rows 16+valid..31, both halves).
+        const int valid = seq - tok0;
+        uint8_t* tile = ring + (size_t)st * kHeadBlockBytes;
+        for (int c = lane; c < (kBlockTokens - valid) * 16; c += 32) {
+          const int row = kBlockTokens + valid + (c >> 4);
+          *reinterpret_cast<uint4*>(tile + ((c >> 3) & 1) * (kHeadBlockBytes / 2) + row * 128 +
+                                    (c & 7) * 16) = make_uint4(0, 0, 0, 0);
+        }
+        __syncwarp();
+      }
 
       // S = Q K^T over 16 tokens: s[j] covers tokens 8j..8j+7.
       float s[2][4];
@@ -169,8 +188,6 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
           mma_bf16_16816(s[j], qa[2 * kp + 1], b2, b3);
         }
       }
-      const int tok0 = (b_begin + i) * kBlockTokens;
-      const bool partial = tok0 + kBlockTokens > seq;
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
 #pragma unroll
@@ -392,7 +409,7 @@ size_t attention_workspace_bytes(int batch, int hq, int hkv, int max_seq_len) {
   const int nblk = (max_seq_len + kBlockTokens - 1) / kBlockTokens;
   int splits = nblk < 1 ? 1 : nblk;
   if (splits > kMaxSplits) splits = kMaxSplits;
-  const size_t counters = ((size_t)batch * hkv * sizeof(int32_t) + 255) & ~size_t(255);
+  const size_t counters = kCounterRegionBytes;
   const size_t lse = ((size_t)batch * hq * splits * sizeof(float) + 255) & ~size_t(255);
   const size_t o = (size_t)batch * hq * splits * kHeadDim * sizeof(float);
   return counters + lse + o;
@@ -405,6 +422,7 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
                                     int max_seq_len, float scale, cudaStream_t stream) {
   if (batch <= 0) return cudaSuccess;
   if (hkv <= 0 || hq % hkv != 0 || hq / hkv > kMaxGroup) return cudaErrorInvalidValue;
+  if ((size_t)batch * hkv * sizeof(int32_t) > kCounterRegionBytes) return cudaErrorInvalidValue;
   cudaError_t e = attn_init_once();
   if (e != cudaSuccess) return e;
   if (workspace_bytes < attention_workspace_bytes(batch, hq, hkv, max_seq_len))
@@ -415,7 +433,7 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
   if (ws_splits > kMaxSplits) ws_splits = kMaxSplits;
 
   uint8_t* ws = static_cast<uint8_t*>(workspace);
-  const size_t counters = ((size_t)batch * hkv * sizeof(int32_t) + 255) & ~size_t(255);
+  const size_t counters = kCounterRegionBytes;
   const size_t lse = ((size_t)batch * hq * ws_splits * sizeof(float) + 255) & ~size_t(255);
 
   AttnArgs a;

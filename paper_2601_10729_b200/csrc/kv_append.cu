@@ -17,6 +17,14 @@
 
 namespace ofb {
 
+// Which (layer, request) rows an append launch touches.  A row is "offloaded"
+// when it has a host slab (host_slabs[l][b] != 0).
+enum AppendMode : int {
+  kAppendResident = 0,   // resident rows only (pool write)
+  kAppendAll = 1,        // every row: host slab (if any) + pool/staging via table
+  kAppendOffloaded = 2,  // offloaded rows only: host slab + staging via table
+};
+
 struct AppendArgs {
   const uint4* k_new;            // [L][B][Hkv][128] bf16
   const uint4* v_new;
@@ -27,7 +35,7 @@ struct AppendArgs {
   int max_blocks;
   int batch;
   int hkv;
-  int device_write_with_host;    // 0: offloaded layers get only the host write
+  int mode;                      // kAppendResident / kAppendAll / kAppendOffloaded
 };
 
 __global__ void __launch_bounds__(256) kv_append_kernel(const AppendArgs a) {
@@ -50,9 +58,10 @@ __global__ void __launch_bounds__(256) kv_append_kernel(const AppendArgs a) {
   const size_t in_block = ((size_t)(h * 2 + kv) * kBlockTokens + slot) * kRowBytes + part * 16;
 
   const uint64_t host = a.host_slabs != nullptr ? a.host_slabs[lb] : 0;
+  if (host != 0 ? a.mode == kAppendResident : a.mode == kAppendOffloaded) return;
   if (host != 0)
     *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(host) + blk_local * block_bytes + in_block) = val;
-  if (a.block_tables != nullptr && (host == 0 || a.device_write_with_host)) {
+  if (a.block_tables != nullptr) {
     const int blk = a.block_tables[lb * a.max_blocks + blk_local];
     if (blk >= 0) *reinterpret_cast<uint4*>(a.pool + blk * block_bytes + in_block) = val;
   }
@@ -61,7 +70,7 @@ __global__ void __launch_bounds__(256) kv_append_kernel(const AppendArgs a) {
 cudaError_t launch_kv_append(const void* k_new, const void* v_new, void* pool,
                              const int32_t* block_tables, int max_blocks,
                              const int32_t* positions, const uint64_t* host_slabs,
-                             int num_layers, int batch, int hkv, bool device_write_with_host,
+                             int num_layers, int batch, int hkv, int mode,
                              cudaStream_t stream) {
   if (batch <= 0 || num_layers <= 0) return cudaSuccess;
   AppendArgs a;
@@ -74,7 +83,7 @@ cudaError_t launch_kv_append(const void* k_new, const void* v_new, void* pool,
   a.max_blocks = max_blocks;
   a.batch = batch;
   a.hkv = hkv;
-  a.device_write_with_host = device_write_with_host ? 1 : 0;
+  a.mode = mode;
   const int warps_per_cta = 8;
   dim3 grid((batch * hkv + warps_per_cta - 1) / warps_per_cta, num_layers);
   kv_append_kernel<<<grid, warps_per_cta * 32, 0, stream>>>(a);

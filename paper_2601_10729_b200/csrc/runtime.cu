@@ -28,7 +28,7 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
 cudaError_t launch_kv_append(const void* k_new, const void* v_new, void* pool,
                              const int32_t* block_tables, int max_blocks,
                              const int32_t* positions, const uint64_t* host_slabs,
-                             int num_layers, int batch, int hkv, bool device_write_with_host,
+                             int num_layers, int batch, int hkv, int mode,
                              cudaStream_t stream);
 int attention_occupancy();
 }  // namespace ofb
@@ -260,7 +260,7 @@ int ofb_kv_append(const void* k_new, const void* v_new, void* kv_pool,
   if (block_tables && !kv_pool) return fail(-1, "ofb_kv_append: block tables need a pool");
   cudaError_t e = ofb::launch_kv_append(k_new, v_new, kv_pool, block_tables, max_blocks,
                                         positions, host_slabs, num_layers, batch, num_kv_heads,
-                                        true, static_cast<cudaStream_t>(stream));
+                                        /*kAppendAll*/ 1, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "kv_append_kernel launch");
   return 0;
 }
@@ -337,9 +337,10 @@ int ofb_runtime_decode_step(ofb_runtime* rt, const ofb_step_desc* d, void* strea
   if (rc) return rc;
   rt->streams_used = nstreams;
 
-  // Step start: a pending migration, then the append of every layer.  Copy
-  // streams start after it: staging from the previous step is released and
-  // host slabs already hold this step's token.
+  // Step start: a pending migration, then the append of every resident row.
+  // Copy streams start after it (staging from the previous step released).
+  // Offloaded rows get their token after their fetch lands (below), so a
+  // fetch moves exactly the b_r blocks the reference's blocks_to_fetch counts.
   if (rt->pending_mig) {
     OFB_CUDA(cudaStreamWaitEvent(cs, rt->mig_done_h2d, 0));
     OFB_CUDA(cudaStreamWaitEvent(cs, rt->mig_done_d2h, 0));
@@ -352,7 +353,7 @@ int ofb_runtime_decode_step(ofb_runtime* rt, const ofb_step_desc* d, void* strea
   }
   cudaError_t e = ofb::launch_kv_append(d->k_new, d->v_new, d->kv_pool, d->block_tables,
                                         d->max_blocks, d->positions, d->host_slabs_dev, L, B,
-                                        d->num_kv_heads, false, cs);
+                                        d->num_kv_heads, /*kAppendResident*/ 0, cs);
   if (e != cudaSuccess) return cuda_fail(e, "kv_append_kernel launch");
   cudaEvent_t ev_start;
   rc = next_sync_event(rt, &ev_start);
@@ -399,10 +400,24 @@ int ofb_runtime_decode_step(ofb_runtime* rt, const ofb_step_desc* d, void* strea
         ++next[b];
       }
     }
-    // Layer l: stall until its own fetches landed (latency.py:185-187), then attend.
+    // Layer l: stall until its own fetches landed (latency.py:185-187), write
+    // the new token into the staged slabs (and their host slabs), then attend.
+    bool layer_fetches = false;
     for (int b = 0; b < B; ++b) {
       cudaEvent_t f = fetch_done[(size_t)l * B + b];
-      if (f) OFB_CUDA(cudaStreamWaitEvent(cs, f, 0));
+      if (f) {
+        OFB_CUDA(cudaStreamWaitEvent(cs, f, 0));
+        layer_fetches = true;
+      }
+    }
+    if (layer_fetches) {
+      const size_t kv_layer = (size_t)B * d->num_kv_heads * ofb::kHeadDim * 2;
+      e = ofb::launch_kv_append(static_cast<const uint8_t*>(d->k_new) + l * kv_layer,
+                                static_cast<const uint8_t*>(d->v_new) + l * kv_layer, d->kv_pool,
+                                d->block_tables + l * bt_layer, d->max_blocks, d->positions,
+                                d->host_slabs_dev + (size_t)l * B, 1, B, d->num_kv_heads,
+                                /*kAppendOffloaded*/ 2, cs);
+      if (e != cudaSuccess) return cuda_fail(e, "kv_append_kernel launch");
     }
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     if (rt->timed) {

@@ -1,0 +1,74 @@
+"""Thin Python handle on the native step runtime (``ofb_runtime``).
+
+The runtime owns the copy streams and events; every call only enqueues work
+(no host blocking) except ``timing()``, which waits on the recorded events.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+class StepRuntime:
+    """K2/K4 copy-engine orchestration + K1/K3 launches for whole steps."""
+
+    def __init__(self, max_copy_streams: int = 16):
+        self.lib = _native.load()
+        handle = self.lib.ofb_runtime_create(max_copy_streams)
+        if not handle:
+            raise _native.NativeError(f"ofb_runtime_create: {self.lib.ofb_last_error().decode()}")
+        self.handle = handle
+
+    def decode_step(self, desc: _native.StepDesc, stream=None) -> None:
+        s = stream if stream is not None else torch.cuda.current_stream()
+        rc = self.lib.ofb_runtime_decode_step(self.handle, ctypes.byref(desc), s.cuda_stream)
+        _native.check(rc, "ofb_runtime_decode_step")
+
+    def migrate(self, dst: np.ndarray, src: np.ndarray, nbytes: np.ndarray, kinds: np.ndarray,
+                record_timing: bool = False, stream=None) -> None:
+        n = len(dst)
+        if n == 0:
+            return
+        dst = np.ascontiguousarray(dst, dtype=np.uint64)
+        src = np.ascontiguousarray(src, dtype=np.uint64)
+        nbytes = np.ascontiguousarray(nbytes, dtype=np.int64)
+        kinds = np.ascontiguousarray(kinds, dtype=np.int32)
+        s = stream if stream is not None else torch.cuda.current_stream()
+        rc = self.lib.ofb_runtime_migrate(self.handle, n, _ptr(dst), _ptr(src), _ptr(nbytes),
+                                          _ptr(kinds), int(record_timing), s.cuda_stream)
+        _native.check(rc, "ofb_runtime_migrate")
+
+    def timing(self) -> dict:
+        t = _native.StepTiming()
+        _native.check(self.lib.ofb_runtime_timing(self.handle, ctypes.byref(t)), "ofb_runtime_timing")
+        return {name: getattr(t, name) for name, _ in _native.StepTiming._fields_}
+
+    def close(self) -> None:
+        if self.handle:
+            self.lib.ofb_runtime_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def link_probe(host_addr: int, dev_addr: int, nbytes: int, reps: int = 10) -> tuple[float, float]:
+    """Best-of-``reps`` pinned H2D / D2H GB/s over ``nbytes``."""
+    lib = _native.load()
+    h2d = ctypes.c_double()
+    d2h = ctypes.c_double()
+    _native.check(lib.ofb_link_probe(host_addr, dev_addr, nbytes, reps, ctypes.byref(h2d),
+                                     ctypes.byref(d2h)), "ofb_link_probe")
+    return h2d.value, d2h.value

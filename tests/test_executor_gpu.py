@@ -1,0 +1,138 @@
+"""The B200 executor under the engine: bit-exact decisions, physical residency
+equal to the BlockTable, every step's attention output vs the CPU oracle,
+byte-exact K4 migrations (evict -> restore round trips) and K2 fetch volume
+equal to the reference's blocks_to_fetch."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2601_10729_b200 import defaults, workload
+from paper_2601_10729_b200.core import PlacementMatrix, RequestState, SloConfig, SystemProfile
+from paper_2601_10729_b200.engine import RunConfig, Simulation
+from paper_2601_10729_b200.latency import blocks_to_fetch
+from paper_2601_10729_b200.policies import PolicyKind, make_policy
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 2e-2, 1e-2
+
+
+def _executor(shape, **kw):
+    from paper_2601_10729_b200.executor import B200Executor
+    return B200Executor(shape, **kw)
+
+
+def _check_step_outputs(ex, batch):
+    """Oracle attention for every (layer, request) of the last step."""
+    L = ex.shape.num_layers
+    pos = ex.last_positions
+    scale = 1.0 / math.sqrt(128)
+    q = ex.last_inputs["q"].float().cpu()
+    out = ex.last_output.float().cpu().numpy()
+    for l in range(L):
+        blocks = [int(p) // 16 + 1 for p in pos]
+        slabs = [ex.slab_bits(r.id, l, n) for r, n in zip(batch, blocks)]
+        pool = np.concatenate(slabs, axis=0)
+        width = max(blocks)
+        bt = np.full((len(batch), width), -1, dtype=np.int32)
+        cur = 0
+        for b, n in enumerate(blocks):
+            bt[b, :n] = np.arange(cur, cur + n)
+            cur += n
+        qb = q[l].to(torch.bfloat16).contiguous().view(torch.int16).numpy().view(np.uint16)
+        want = oracle.decode_attention(qb, pool, bt, (pos + 1).astype(np.int32), scale)
+        for b, r in enumerate(batch):
+            where = (f"layer {l} request {r.id} ({ex.residency(r.id)[l]}) pos {pos[b]}: "
+                     f"gpu nan {np.isnan(out[l, b]).any()} oracle nan {np.isnan(want[b]).any()}")
+            np.testing.assert_allclose(out[l, b], want[b], rtol=RTOL, atol=ATOL, err_msg=where)
+
+
+def test_engine_with_executor_is_bit_exact_and_correct():
+    from paper_2601_10729_b200.executor import B200Executor, ModelShape
+
+    prof = SystemProfile(num_layers=4, compute_base_ms=0.2, compute_per_token_ms=0.0004,
+                         bandwidth_blocks_per_ms=12.0, gpu_block_budget=120, block_size=16,
+                         prefill_per_token_ms=0.001)
+    slo = SloConfig(tbt_target_ms=2.5, tpot_target_ms=2.5, window_min=2, window_max=6)
+    trace = workload.Trace(tuple(workload.TraceRequest(i * 3, 90 + 37 * i, 6 + i % 3)
+                                 for i in range(6)), {})
+    cfg = RunConfig(max_batch=3)
+
+    def run(executor):
+        policy = make_policy(PolicyKind.ORBIT, prof, slo, max_batch=3, token_cap=cfg.batch_token_cap)
+        sim = Simulation(trace, policy, prof, slo, cfg, executor=executor)
+        return sim, sim.execute()
+
+    _, ref_log = run(None)
+
+    class Checked(B200Executor):
+        steps_checked = 0
+
+        def decode_step(self, batch, placement=None, inputs=None):
+            ms = super().decode_step(batch, placement, inputs)
+            for req, row in zip(batch, placement.rows):
+                assert self.residency(req.id) == ["dev" if b else "host" for b in row]
+            _check_step_outputs(self, batch)
+            Checked.steps_checked += 1
+            return ms
+
+    ex = Checked.for_trace(trace, prof, shape=ModelShape(4, 8, 2), max_batch=3, record_timing=True)
+    _, log = run(ex)
+    stripped = [dict(r, payload={k: v for k, v in r["payload"].items() if k != "measured_us"})
+                if r["kind"] == "step" else r for r in log]
+    assert stripped == ref_log
+    assert Checked.steps_checked == sum(1 for r in log if r["kind"] == "step")
+    assert any(0 in row for r in log if r["kind"] == "step" for row in r["payload"]["rows"])
+    assert ex.migrated["moves"] >= 0
+    ex.close()
+
+
+def test_cfg1_plan_fetch_volume_and_outputs():
+    from paper_2601_10729_b200.executor import TOY
+
+    batch = [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=4088, target_output_tokens=64)
+             for i in range(4)]
+    placement = PlacementMatrix((0, 1, 2, 3), 4, ((0, 0, 0, 0), (0, 0, 0, 0), (1, 1, 1, 1), (1, 1, 1, 1)))
+    ex = _executor(TOY, device_blocks=4 * 4 * 262 + 8 * 262, host_blocks=4 * 4 * 262 + 16,
+                   record_timing=True)
+    ex.install(batch, placement)
+    for _ in range(3):
+        ex.decode_step(batch, placement)
+        _check_step_outputs(ex, batch)
+        t = ex.last_timing
+        assert t["copies"] == 8
+        assert t["copy_bytes"] == blocks_to_fetch(placement, batch) * TOY.block_bytes
+        for r in batch:
+            r.record_generated_token()
+    ex.close()
+
+
+@pytest.mark.parametrize("slots", [1, 2])
+def test_reconfiguration_round_trip_is_byte_exact(slots):
+    from paper_2601_10729_b200.executor import ModelShape
+
+    shape = ModelShape(6, 8, 2)
+    batch = [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=300 + 50 * i,
+                          target_output_tokens=40) for i in range(3)]
+    ex = _executor(shape, device_blocks=6 * 3 * 30 + 64, host_blocks=6 * 3 * 30 + 64,
+                   staging_slots=slots)
+    a = PlacementMatrix.from_strides([0, 1, 2], 6, [2, 3, None])
+    b = PlacementMatrix.from_strides([0, 1, 2], 6, [3, None, 1])
+    ex.install(batch, a)
+    for _ in range(2):
+        ex.decode_step(batch, a)
+        for r in batch:
+            r.record_generated_token()
+    before = {(r.id, l): ex.slab_bits(r.id, l, r.blocks_per_layer) for r in batch for l in range(6)}
+    ex.install(batch, b)          # evicts and restores layers (K4)
+    ex.install(batch, a)          # and back
+    after = {(r.id, l): ex.slab_bits(r.id, l, r.blocks_per_layer) for r in batch for l in range(6)}
+    for key in before:
+        np.testing.assert_array_equal(before[key], after[key])
+    ex.decode_step(batch, a)
+    _check_step_outputs(ex, batch)
+    ex.close()

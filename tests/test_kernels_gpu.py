@@ -110,3 +110,18 @@ def test_append_then_attend_sees_new_token():
     want = oracle.decode_attention(bf16_bits(case["q"]), host_pool, case["block_tables"], pos + 1,
                                    case["scale"])
     np.testing.assert_allclose(got.float().cpu().numpy(), want, rtol=RTOL, atol=ATOL)
+
+
+def test_garbage_past_sequence_end_is_ignored():
+    # NaN bit patterns in the unused slots of the last block must not leak
+    # into the output (P is 0 there, but 0 * NaN = NaN in a P.V tile).
+    case = make_case([33, 16 * 5 + 1, 7], 8, 2, seed=9)
+    pool = case["pool"].clone()
+    bits = pool.view(torch.int16)
+    for b, seq in enumerate(case["seq_lens"]):
+        blk = case["block_tables"][b][(seq - 1) // 16]
+        bits[blk, :, :, (seq % 16 or 16):, :] = 0x7FC0          # bf16 quiet NaN
+    case["pool"] = pool
+    got = _run_gpu(case)
+    assert not np.isnan(got).any()
+    np.testing.assert_allclose(got, _run_oracle(case), rtol=RTOL, atol=ATOL)
