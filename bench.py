@@ -105,6 +105,23 @@ def _measured_peaks():
         return {}
 
 
+def _ncu_traffic(alg_bytes):
+    """DRAM bytes per K1 launch from the committed ncu --set full capture of the
+    same layer shape (profiles/), scaled to this launch's algorithmic bytes."""
+    for path in sorted((ROOT / "profiles").glob("*k1_ncu_full_cfg2layer.json"), reverse=True):
+        try:
+            rec = json.loads(path.read_text())[0]
+            unit = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
+            rd = float(rec["dram__bytes_read.sum"][0]) * unit[rec["dram__bytes_read.sum"][1]]
+            wr = float(rec["dram__bytes_write.sum"][0]) * unit[rec["dram__bytes_write.sum"][1]]
+            captured_alg = 16 * 32768 * 8 * 2 * 128 * 2 + 2 * 16 * 32 * 128 * 2
+            return {"bytes": (rd + wr) * alg_bytes / captured_alg,
+                    "ratio_to_algorithmic": (rd + wr) / captured_alg, "source": path.name}
+        except Exception:
+            continue
+    return None
+
+
 def build_batch(cfg):
     from paper_2601_10729_b200.core import PlacementMatrix, RequestState
 
@@ -287,7 +304,8 @@ def run_ours(args, cfg):
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
 
-    # e2e through the public API with host buffers
+    # e2e through the public API with host buffers (one untimed warm-up step)
+    step(0, e2e=True)
     barrier()
     e0 = time.perf_counter()
     e2e_steps = max(2, args.steps // 2)
@@ -319,6 +337,7 @@ def run_ours(args, cfg):
     copy_span = statistics.median(t["copy_span_ms"] for t in timings)
     bound = "host_link" if host_alg / h2d_peak > hbm_alg / hbm_peak else "hbm"
 
+    traffic = _ncu_traffic(attn_bytes)
     value = B / (ms_per_step * 1e-3)  # whole job: every rank serves the same B tokens (TP)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -353,7 +372,10 @@ def run_ours(args, cfg):
                 "h2d_bytes_per_step": h2d_in, "d2h_bytes_per_step": d2h_out},
         "roofline": {"bound": "hbm", "kernel": "paged_gqa_decode_kernel (K1)",
                      "achieved": attn_gbs, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": attn_gbs / hbm_peak, "traffic": None,
+                     "frac": attn_gbs / hbm_peak,
+                     "traffic": (traffic or {}).get("bytes"),
+                     "traffic_over_algorithmic": (traffic or {}).get("ratio_to_algorithmic"),
+                     "traffic_source": (traffic or {}).get("source"),
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
                      "bytes_per_launch": attn_bytes, "launch_ms": attn_ms,
                      "frac_of_8tbs_nominal": attn_gbs / 8000.0},
@@ -380,18 +402,158 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
+def run_reconfig(args):
+    """Config 5: plan change stride 2 <-> stride 4 on the 8B shape, sweep B x T.
+
+    Each point installs stride 2, decodes, switches to stride 4 (H2D restore of
+    the layers = 2 mod 4: reconfiguration_delta = (8*b_r, 0) per request) and back
+    (D2H eviction of the same layers), decoding one step after each switch.
+    Migration GB/s per direction is measured with CUDA events on the runtime's
+    migration streams; the reference only charges h2d_blocks / bandwidth
+    (src/engine.py:248) and treats D2H as free.
+    """
+    import torch
+
+    from paper_2601_10729_b200.core import PlacementMatrix, RequestState
+    from paper_2601_10729_b200.executor import B200Executor, LLAMA31_8B
+    from paper_2601_10729_b200.latency import reconfiguration_delta
+    from paper_2601_10729_b200.runtime import link_probe
+
+    shape = LLAMA31_8B
+    max_tokens = args.sweep_max_tokens
+    points = [(b, t) for b in (1, 2, 4, 8, 16, 32, 64) for t in (16384, 32768, 65536, 131072)
+              if b * t <= max_tokens]
+    cap_of = lambda t: -(-(t + 64 + 1) // 16)  # noqa: E731
+    dev_blocks = max(int(0.75 * b * shape.num_layers * cap_of(t)) + b * cap_of(t) for b, t in points) + 64
+    host_blocks = max(b * (shape.num_layers // 2) * cap_of(t) for b, t in points) + 64
+    ex = B200Executor(shape, device_blocks=dev_blocks, host_blocks=host_blocks, record_timing=True,
+                      fill="zeros")
+    h2d_peak, d2h_peak = link_probe(ex.host.base, ex.pool.base, 1 << 30, 10)
+    results = []
+    for b, t in points:
+        batch = [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=t - 8, target_output_tokens=64)
+                 for i in range(b)]
+        ids = [r.id for r in batch]
+        s2 = PlacementMatrix.from_strides(ids, shape.num_layers, [2] * b)
+        s4 = PlacementMatrix.from_strides(ids, shape.num_layers, [4] * b)
+        ex.install(batch, s2)
+        base_ms = ex.decode_step(batch, s2)
+        rec = {"batch": b, "context": t}
+        for name, old, new in (("restore_h2d", s2, s4), ("evict_d2h", s4, s2)):
+            up, down = reconfiguration_delta(old, new, batch)
+            ex.install(batch, new)
+            tm = ex.runtime.timing()
+            step_ms = ex.decode_step(batch, new)
+            nbytes = tm["mig_h2d_bytes"] + tm["mig_d2h_bytes"]
+            rec[name] = {"delta_blocks": [up, down], "bytes": nbytes, "ms": tm["mig_ms"],
+                         "GBps": nbytes / (tm["mig_ms"] * 1e-3) / 1e9 if tm["mig_ms"] else None,
+                         "frac_of_link_peak": (nbytes / (tm["mig_ms"] * 1e-3) / 1e9)
+                         / (h2d_peak if up else d2h_peak) if tm["mig_ms"] else None,
+                         "model_charge_ms": up * shape.block_bytes / (h2d_peak * 1e6),
+                         "next_step_ms": step_ms}
+        rec["step_ms_stride2"] = base_ms
+        results.append(rec)
+        for r in batch:
+            ex.release(r.id)
+        torch.cuda.synchronize()
+    line = {"metric": "plan-change migration GB/s per direction (config 5)", "config": "cfg5",
+            "h2d_peak_gbs": h2d_peak, "d2h_peak_gbs": d2h_peak, "points": results}
+    print(json.dumps(line), flush=True)
+    ex.close()
+
+
+def cfg3_setup(args):
+    """Config 3: 8B shape, mixed 8K-128K trace, OrbitPolicy with online refinement
+    and fallback deferral, B200-calibrated profile."""
+    from paper_2601_10729_b200 import defaults, workload
+    from paper_2601_10729_b200.calibrate import b200_profile
+    from paper_2601_10729_b200.engine import RunConfig
+
+    spec = workload.LengthSpec(kind="lognormal", prompt_median=32768, prompt_sigma=0.6,
+                               output_median=args.cfg3_output_median, output_sigma=0.5,
+                               max_prompt=131072, max_output=4 * args.cfg3_output_median)
+    raw = workload.generate(seed=3, rate=30.0, cv=1.5, length_spec=spec, count=args.cfg3_requests)
+    # builder-side min-8K filter (SURVEY.md 8(d) cfg3)
+    trace = workload.Trace(tuple(workload.TraceRequest(r.arrival_ms, max(r.prompt_tokens, 8192),
+                                                       r.output_tokens) for r in raw.requests),
+                           dict(raw.metadata, min_prompt="8192"))
+    profile = b200_profile(32, 8, gpu_block_budget=args.cfg3_budget_blocks)
+    slo = defaults.default_slo(profile, scale=args.slo_scale)
+    cfg = RunConfig(max_batch=4, batch_token_cap=600000)
+    return trace, profile, slo, cfg
+
+
+def run_cfg3(args):
+    import torch
+
+    from paper_2601_10729_b200.engine import Simulation
+    from paper_2601_10729_b200.executor import B200Executor, LLAMA31_8B
+    from paper_2601_10729_b200.metrics import collect_metrics
+    from paper_2601_10729_b200.policies import PolicyKind, make_policy
+
+    trace, profile, slo, cfg = cfg3_setup(args)
+
+    def simulate(executor, mode):
+        policy = make_policy(PolicyKind.ORBIT, profile, slo, max_batch=cfg.max_batch,
+                             token_cap=cfg.batch_token_cap)
+        sim = Simulation(trace, policy, profile, slo, cfg, executor=executor, mode=mode)
+        t0 = time.perf_counter()
+        log = sim.execute()
+        return log, time.perf_counter() - t0
+
+    model_log, model_s = simulate(None, "parity")
+    out = {"metric": METRIC, "config": "cfg3",
+           "workload": "Llama-3.1-8B shape, mixed 8K-128K lognormal trace (seed 3), OrbitPolicy, "
+                       f"max_batch 4, HBM budget {profile.gpu_block_budget} blocks x 64 KiB",
+           "requests": len(trace.requests),
+           "prompts": [r.prompt_tokens for r in trace.requests]}
+    steps_model = [r for r in model_log if r["kind"] == "step"]
+    out["host_control_ms_per_step"] = model_s * 1e3 / max(1, len(steps_model))
+    for mode in ("parity", "live"):
+        ex = B200Executor.for_trace(trace, profile, shape=LLAMA31_8B, max_batch=cfg.max_batch)
+        log, wall_s = simulate(ex, mode)
+        steps = [r for r in log if r["kind"] == "step"]
+        gpu_ms = sum(r["payload"]["measured_us"] for r in steps) / 1e3
+        tokens = sum(len(r["payload"]["ids"]) for r in steps)
+        rep = collect_metrics(log)
+        rec = {"steps": len(steps), "tokens": tokens, "gpu_ms": gpu_ms,
+               "tokens_per_s_gpu": tokens / (gpu_ms * 1e-3), "wall_s": wall_s,
+               "tpot_attainment": rep.tpot_attainment, "tbt_attainment": rep.tbt_attainment,
+               "tbt_p95_ms": rep.tbt_p95_ms, "pauses": rep.pauses, "resumes": rep.resumes,
+               "replans": rep.replans, "migrated": dict(ex.migrated)}
+        if mode == "parity":
+            stripped = [dict(r, payload={k: v for k, v in r["payload"].items() if k != "measured_us"})
+                        if r["kind"] == "step" else r for r in log]
+            rec["decisions_match_model_run"] = stripped == model_log
+            rec["model_tpot_attainment"] = collect_metrics(model_log).tpot_attainment
+        out[mode] = rec
+        ex.close()
+        torch.cuda.synchronize()
+    print(json.dumps(out), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
+    ap.add_argument("--config", choices=sorted(CONFIGS) + ["cfg3", "cfg5"], default="cfg2")
+    ap.add_argument("--slo-scale", type=float, default=1.5)
+    ap.add_argument("--cfg3-requests", type=int, default=10)
+    ap.add_argument("--cfg3-output-median", type=int, default=48)
+    ap.add_argument("--cfg3-budget-blocks", type=int, default=100000)
     ap.add_argument("--staging-slots", type=int, default=1)
     ap.add_argument("--copy-streams", type=int, default=16)
     ap.add_argument("--ref-seconds", type=float, default=3.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep-max-tokens", type=int, default=524288,
+                    help="cfg5: largest B x T swept (KV bytes = tokens x 128 KiB)")
     args = ap.parse_args()
+    if args.config == "cfg5":
+        return run_reconfig(args)
+    if args.config == "cfg3":
+        return run_cfg3(args)
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference_arm(args, cfg)

@@ -104,7 +104,7 @@ class B200Executor:
         self.last_output: torch.Tensor | None = None
         self.migrated = {"h2d_bytes": 0, "d2h_bytes": 0, "moves": 0}
         self._ws = None
-        self._workspace_key = None
+        self._mig_start = None        # event before the last un-stepped migration
 
     # ------------------------------------------------------------ sizing
     @classmethod
@@ -190,6 +190,9 @@ class B200Executor:
                         evicted.append((st.dev[layer], st.capacity))
                         st.dev[layer] = None
         if moves:
+            if self._mig_start is None:
+                self._mig_start = torch.cuda.Event(enable_timing=True)
+                self._mig_start.record(torch.cuda.current_stream())
             arr = np.array(moves, dtype=np.uint64)
             self.runtime.migrate(arr[:, 0], arr[:, 1], arr[:, 2].astype(np.int64),
                                  arr[:, 3].astype(np.int32), record_timing=self.record_timing)
@@ -329,9 +332,12 @@ class B200Executor:
                     raise RuntimeError("physical residency does not match the placement")
         desc, keep = self.prepare_step(batch, inputs)
         stream = torch.cuda.current_stream()
-        t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
+        if self._mig_start is not None:   # the step also waits for its plan's migration
+            t0, self._mig_start = self._mig_start, None
+        else:
+            t0 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
         self.runtime.decode_step(desc, stream)
         t1.record(stream)
         t1.synchronize()
