@@ -39,11 +39,17 @@ PCIE5_NOMINAL_GBS = 63.0
 CONFIGS = {
     # name: (layers, hq, hkv, batch, prompt, stride, output)
     "cfg1": dict(layers=4, hq=8, hkv=2, batch=4, prompt=4088, strides=[1, 1, None, None],
-                 output=64, workload="toy 4-layer GQA (8q/2kv, d=128), B=4, 4K ctx, reference "
+                 output=64, hidden=1024, workload="toy 4-layer GQA (8q/2kv, d=128), B=4, 4K ctx, reference "
                                      "solve plan: requests 0,1 fully host-resident"),
     "cfg2": dict(layers=32, hq=32, hkv=8, batch=16, prompt=32760, strides=[2] * 16, output=64,
+                 hidden=4096,
                  workload="Llama-3.1-8B shape (32 layers, 32q/8kv, d=128, bf16), B=16, 32K ctx, "
                           "stride-2 plan: 50% of layers' KV host-resident, 1xB200"),
+    "cfg4": dict(layers=80, hq=64, hkv=8, batch=32, prompt=65528, strides="flexgen_plus",
+                 output=64, hidden=8192,
+                 workload="Llama-3.1-70B shape (80 layers, 64q/8kv, d=128, bf16), B=32, 64K ctx, "
+                          "KV-head sharded TP, per-layer o-proj + all-reduce, plan = "
+                          "plan_flexgen_plus under each rank's HBM budget"),
 }
 
 
@@ -98,6 +104,34 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def _probe_link(dev, nbytes: int = 1 << 30, reps: int = 10):
+    """Best-of-10 pinned 1 GiB cudaMemcpyAsync H2D / D2H on this GPU."""
+    import torch
+
+    from paper_2601_10729_b200 import _native
+    from paper_2601_10729_b200.runtime import link_probe
+
+    lib = _native.load()
+    host = lib.ofb_host_alloc(nbytes)
+    if not host:
+        raise RuntimeError("pinned probe buffer allocation failed")
+    try:
+        d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        return link_probe(host, d.data_ptr(), nbytes, reps)
+    finally:
+        lib.ofb_host_free(host)
+
+
+def _mem_available() -> int:
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 1 << 40
+
+
 def _measured_peaks():
     try:
         return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -122,11 +156,20 @@ def _ncu_traffic(alg_bytes):
     return None
 
 
-def build_batch(cfg):
+def build_batch(cfg, shape=None, hbm_budget_bytes=None):
+    """Batch + placement.  Fixed stride lists come from the config; "flexgen_plus"
+    asks the reference-exact baseline planner (src/policies.py:132-137) for the
+    best uniform stride under this rank's HBM budget."""
+    from paper_2601_10729_b200.calibrate import b200_profile
     from paper_2601_10729_b200.core import PlacementMatrix, RequestState
+    from paper_2601_10729_b200.policies import plan_flexgen_plus
 
     batch = [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=cfg["prompt"],
                           target_output_tokens=cfg["output"]) for i in range(cfg["batch"])]
+    if cfg["strides"] == "flexgen_plus":
+        budget = int(hbm_budget_bytes // shape.block_bytes)
+        profile = b200_profile(cfg["layers"], shape.num_kv_heads, budget)
+        return batch, plan_flexgen_plus(batch, profile)
     placement = PlacementMatrix.from_strides([r.id for r in batch], cfg["layers"], cfg["strides"])
     return batch, placement
 
@@ -236,25 +279,43 @@ def run_ours(args, cfg):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
+    from paper_2601_10729_b200.tp import HeadShard, TensorParallelDecoder
+
     hkv_total, hq_total = cfg["hkv"], cfg["hq"]
-    if hkv_total % world:
-        raise SystemExit(f"KV heads ({hkv_total}) must divide by the GPU count ({world})")
+    tp = world if world > 1 else max(1, args.tp_emulate)
+    if hkv_total % tp:
+        raise SystemExit(f"KV heads ({hkv_total}) must divide by the TP degree ({tp})")
     # KV-head sharding: each rank owns Hkv/N KV heads + their q heads
-    shape = ModelShape(cfg["layers"], hq_total // world, hkv_total // world)
-    batch, placement = build_batch(cfg)
+    shard = HeadShard(rank if world > 1 else 0, tp, hq_total, hkv_total)
+    shape = ModelShape(cfg["layers"], shard.local_q, shard.local_kv)
     L, B = cfg["layers"], cfg["batch"]
     cap = -(-(cfg["prompt"] + cfg["output"] + 1) // 16)
+    slots = args.staging_slots
+    use_tp = world > 1 or args.tp_emulate > 1 or cfg["strides"] == "flexgen_plus"
+    # per-rank HBM left for KV: total - o-proj shard - staging - workspace/slack
+    free_b, _total_b = torch.cuda.mem_get_info(dev)
+    oproj_bytes = L * shard.local_q * 128 * cfg["hidden"] * 2 if use_tp else 0
+    staging_bytes = B * slots * cap * shape.block_bytes
+    kv_budget = free_b - oproj_bytes - staging_bytes - (6 << 30)
+    batch, placement = build_batch(cfg, shape, kv_budget)
     n_off = sum(row.count(0) for row in placement.rows)
     n_res = L * B - n_off
-    slots = args.staging_slots
+    host_need = n_off * cap * shape.block_bytes
+    avail = _mem_available() // max(1, world)
+    if host_need > 0.85 * avail:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "config": {"workload": cfg["workload"]},
+                              "n_gpus": world, "tp": tp, "unavailable":
+                              f"needs {host_need / 2**30:.0f} GiB pinned host KV per rank, "
+                              f"{avail / 2**30:.0f} GiB available"}), flush=True)
+        return
     device_blocks = n_res * cap + B * slots * cap + 16
     host_blocks = max(n_off * cap, 1) + 16
     ex = B200Executor(shape, device=dev, device_blocks=device_blocks, host_blocks=host_blocks,
                       staging_slots=slots, copy_streams=args.copy_streams, seed=rank,
                       record_timing=True)
     # host-link peaks on this GPU (1 GiB pinned, best of 10) - before the data lands
-    probe_bytes = min(1 << 30, ex.host.nbytes, ex.pool.tensor.numel() * 2)
-    h2d_peak, d2h_peak = link_probe(ex.host.base, ex.pool.base, probe_bytes, 10)
+    h2d_peak, d2h_peak = _probe_link(dev)
     ex.install(batch, placement)
     torch.cuda.synchronize()
 
@@ -264,18 +325,25 @@ def run_ours(args, cfg):
 
     attn_tokens = []
 
+    tpd = TensorParallelDecoder(ex, shard, cfg["hidden"], seed=0) if use_tp else None
+
+    def run_step(inp):
+        if tpd is not None:
+            tpd.step(batch, inp)
+        else:
+            ex.decode_step(batch, None, inp, sync=False)
+
     def step(i, e2e=False):
         attn_tokens.append(sum(r.total_tokens + 1 for r in batch))
-        if e2e:
+        if e2e:   # a serving loop: inputs from host, result read back before the next step
             dev_in = {k: v.to(dev, non_blocking=True) for k, v in pinned[i % 2].items()}
-            ms = ex.decode_step(batch, None, dev_in)
+            run_step(dev_in)
             out_host.copy_(ex.last_output, non_blocking=True)
             torch.cuda.current_stream().synchronize()
-        else:
-            ms = ex.decode_step(batch, None, inputs[i % 2])
+        else:     # device-resident inputs, steps pipelined (host prepares N+1 during N)
+            run_step(inputs[i % 2])
         for r in batch:
             r.record_generated_token()
-        return ms
 
     def barrier():
         if dist is not None:
@@ -284,20 +352,21 @@ def run_ours(args, cfg):
 
     for i in range(args.warmup):
         step(i)
+    ex.drain()
     barrier()
+    ex.runtime.timing_reset()
     attn_tokens.clear()
-    timings = []
-    steps_ms = []
     with ClockSampler(local) as clocks:
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record()
         for i in range(args.steps):
-            steps_ms.append(step(i))
-            timings.append(dict(ex.last_timing))
+            step(i)
         t_end.record()
+        ex.drain()
         barrier()
     total_ms = t_start.elapsed_time(t_end)
+    tm = ex.runtime.timing()   # per-launch K1 events + fetch bytes, accumulated over the timed steps
     if dist is not None:
         t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -323,7 +392,7 @@ def run_ours(args, cfg):
     # roofline of K1 (dominant kernel): algorithmic bytes per launch / event duration
     peaks = _measured_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    attn_ms = sum(t["attn_ms_total"] for t in timings) / sum(t["layers"] for t in timings)
+    attn_ms = tm["acc_attn_ms"] / tm["acc_attn_launches"]
     tokens_per_layer = sum(attn_tokens[: args.steps]) / args.steps
     kv_bytes = tokens_per_layer * shape.kv_bytes_per_token
     qo_bytes = 2 * B * shape.num_q_heads * 128 * 2
@@ -331,10 +400,10 @@ def run_ours(args, cfg):
     attn_gbs = attn_bytes / (attn_ms * 1e-3) / 1e9
 
     # step roofline: host link (HOST_alg) vs HBM (HBM_alg), SURVEY.md 8(d)
-    host_alg = timings[-1]["copy_bytes"]
+    host_alg = tm["acc_copy_bytes"] / tm["acc_steps"]
     hbm_alg = L * attn_bytes + B * L * shape.kv_bytes_per_token
     roof_ms = max(hbm_alg / (hbm_peak * 1e9), host_alg / (h2d_peak * 1e9)) * 1e3
-    copy_span = statistics.median(t["copy_span_ms"] for t in timings)
+    copy_span = tm["copy_span_ms"]
     bound = "host_link" if host_alg / h2d_peak > hbm_alg / hbm_peak else "hbm"
 
     traffic = _ncu_traffic(attn_bytes)
@@ -364,9 +433,13 @@ def run_ours(args, cfg):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) KV, q)",
         "config": {"workload": cfg["workload"], "global_batch": B, "seq_len": cfg["prompt"],
                    "layers": L, "q_heads": hq_total, "kv_heads": hkv_total,
-                   "parallelism": f"tp{world} (KV-head sharded)" if world > 1 else "single GPU",
+                   "parallelism": (f"tp{world} (KV-head sharded, o-proj all-reduce per layer)"
+                                   if world > 1 else
+                                   f"tp{tp} rank-0 shard emulated on 1 GPU (no collective)"
+                                   if tp > 1 else "single GPU"),
+                   "placement_rows_offloaded": [row.count(0) for row in placement.rows][:4],
                    "offloaded_slabs": n_off, "staging_slots": slots,
-                   "copy_streams": timings[-1]["copy_streams"],
+                   "copy_streams": tm["copy_streams"], "host_pipelining": "4 steps in flight",
                    "l2": "inputs (64 GiB KV) larger than the 126 MB L2; no flush needed"},
         "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": h2d_in, "d2h_bytes_per_step": d2h_out},
@@ -385,7 +458,8 @@ def run_ours(args, cfg):
                           "h2d_peak_gbs": h2d_peak, "d2h_peak_gbs": d2h_peak,
                           "host_link_gbs": host_alg / (ms_per_step * 1e-3) / 1e9,
                           "copy_span_ms": copy_span,
-                          "copy_gbs_during_span": host_alg / (copy_span * 1e-3) / 1e9,
+                          "copy_gbs_during_span": (host_alg / (copy_span * 1e-3) / 1e9
+                                                   if copy_span else None),
                           "frac_of_pcie5_nominal": host_alg / (ms_per_step * 1e-3) / 1e9
                           / PCIE5_NOMINAL_GBS,
                           "blocks_to_fetch_check": blocks_to_fetch(placement, batch)},
@@ -428,7 +502,7 @@ def run_reconfig(args):
     host_blocks = max(b * (shape.num_layers // 2) * cap_of(t) for b, t in points) + 64
     ex = B200Executor(shape, device_blocks=dev_blocks, host_blocks=host_blocks, record_timing=True,
                       fill="zeros")
-    h2d_peak, d2h_peak = link_probe(ex.host.base, ex.pool.base, 1 << 30, 10)
+    h2d_peak, d2h_peak = _probe_link(ex.device)
     results = []
     for b, t in points:
         batch = [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=t - 8, target_output_tokens=64)
@@ -543,10 +617,13 @@ def main():
     ap.add_argument("--cfg3-requests", type=int, default=10)
     ap.add_argument("--cfg3-output-median", type=int, default=48)
     ap.add_argument("--cfg3-budget-blocks", type=int, default=100000)
-    ap.add_argument("--staging-slots", type=int, default=1)
+    ap.add_argument("--staging-slots", type=int, default=2,
+                    help="1 = reference single-slot launch rule, 2 = double-buffered staging")
     ap.add_argument("--copy-streams", type=int, default=16)
     ap.add_argument("--ref-seconds", type=float, default=3.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tp-emulate", type=int, default=1,
+                    help="run rank 0's KV-head shard of a TP-N deployment on one GPU")
     ap.add_argument("--sweep-max-tokens", type=int, default=524288,
                     help="cfg5: largest B x T swept (KV bytes = tokens x 128 KiB)")
     args = ap.parse_args()

@@ -128,6 +128,9 @@ typedef struct ofb_step_timing {
   int32_t copy_streams;     /* copy streams used */
   float mig_ms;             /* last ofb_runtime_migrate span (0 if none timed) */
   double mig_h2d_bytes, mig_d2h_bytes;
+  /* accumulated over every timed step since the last ofb_runtime_timing_reset */
+  int32_t acc_steps, acc_attn_launches;
+  double acc_attn_ms, acc_copy_bytes, acc_step_ms;
 } ofb_step_timing;
 
 OFB_API ofb_runtime* ofb_runtime_create(int32_t max_copy_streams);
@@ -147,18 +150,37 @@ OFB_API int ofb_runtime_destroy(ofb_runtime* rt);
  * kvsim/engine.py:715-734 with the execution it prices. */
 OFB_API int ofb_runtime_decode_step(ofb_runtime* rt, const ofb_step_desc* desc, void* stream);
 
+/* The same step split in three so a caller can interleave per-layer work of
+ * its own on `stream` (e.g. a tensor-parallel o-projection + all-reduce after
+ * each layer's attention): begin (step-start append, copy streams armed),
+ * layers(count) (fetches + staging append + attention of the next `count`
+ * layers), end.  The host arrays of `desc` must stay valid until end. */
+OFB_API int ofb_runtime_step_begin(ofb_runtime* rt, const ofb_step_desc* desc, void* stream);
+OFB_API int ofb_runtime_step_layers(ofb_runtime* rt, int32_t count);
+OFB_API int ofb_runtime_step_end(ofb_runtime* rt);
+
 /* K4: plan-change reconfiguration.  Enqueue n whole-slab moves
  * (kind 0 = host->device restore, 1 = device->host eviction, 2 = device->device)
- * on the migration streams after all work already on `stream`; `stream` (and
- * the next decode step's copy streams) then wait for them.  Realises
+ * on the migration streams after all work already on `stream`.  `stream` (and
+ * the next decode step) then waits for the restores; evictions overlap the next
+ * step and only fetches of a slab still being evicted wait for them.  Realises
  * apply_plan (kvsim/engine.py:213-248), BlockTable.evict_for_space
  * (kvsim/engine.py:184-204) and reconfiguration_delta (kvsim/latency.py:277-297). */
 OFB_API int ofb_runtime_migrate(ofb_runtime* rt, int32_t n, const uint64_t* dst, const uint64_t* src,
                         const int64_t* bytes, const int32_t* kinds, int32_t record_timing,
                         void* stream);
 
-/* Timing of the last decode step / migration (synchronises on their events). */
+/* 1 while the last migration batch's evictions (D2H) are still in flight, else 0;
+ * with wait != 0 it first blocks until they land.  Evicted HBM extents may be
+ * reused only after this returns 0.  Restores (H2D) are always complete before
+ * later work on the compute stream. */
+OFB_API int ofb_runtime_migration_pending(ofb_runtime* rt, int32_t wait);
+
+/* Timing of the last timed decode step / migration plus totals over all timed
+ * steps (synchronises on their events; steps are timed into a 4-deep ring, so
+ * the host can keep enqueuing without waiting). */
 OFB_API int ofb_runtime_timing(ofb_runtime* rt, ofb_step_timing* out);
+OFB_API int ofb_runtime_timing_reset(ofb_runtime* rt);
 
 /* Host-link probe: best-of-reps pinned cudaMemcpyAsync in each direction. */
 OFB_API int ofb_link_probe(void* host, void* dev, int64_t bytes, int32_t reps, double* h2d_gbs,

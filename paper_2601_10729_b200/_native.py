@@ -50,6 +50,8 @@ class StepTiming(ctypes.Structure):
         ("copies", c_i32), ("copy_ms_sum", c_f32), ("copy_bytes", c_f64),
         ("copy_span_ms", c_f32), ("step_ms", c_f32), ("copy_streams", c_i32),
         ("mig_ms", c_f32), ("mig_h2d_bytes", c_f64), ("mig_d2h_bytes", c_f64),
+        ("acc_steps", c_i32), ("acc_attn_launches", c_i32), ("acc_attn_ms", c_f64),
+        ("acc_copy_bytes", c_f64), ("acc_step_ms", c_f64),
     ]
 
 
@@ -68,8 +70,13 @@ SIGNATURES = {
     "ofb_runtime_create": (c_vp, [c_i32]),
     "ofb_runtime_destroy": (ctypes.c_int, [c_vp]),
     "ofb_runtime_decode_step": (ctypes.c_int, [c_vp, ctypes.POINTER(StepDesc), c_vp]),
+    "ofb_runtime_step_begin": (ctypes.c_int, [c_vp, ctypes.POINTER(StepDesc), c_vp]),
+    "ofb_runtime_step_layers": (ctypes.c_int, [c_vp, c_i32]),
+    "ofb_runtime_step_end": (ctypes.c_int, [c_vp]),
     "ofb_runtime_migrate": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "ofb_runtime_timing": (ctypes.c_int, [c_vp, ctypes.POINTER(StepTiming)]),
+    "ofb_runtime_migration_pending": (ctypes.c_int, [c_vp, c_i32]),
+    "ofb_runtime_timing_reset": (ctypes.c_int, [c_vp]),
     "ofb_link_probe": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, ctypes.POINTER(c_f64),
                                       ctypes.POINTER(c_f64)]),
 }

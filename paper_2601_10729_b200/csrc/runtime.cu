@@ -121,28 +121,64 @@ struct CopyTiming {
   int stream;
 };
 
+// Timing events of one step.  Steps are timed into a ring of records so the
+// host never has to wait on step N to enqueue step N+1; a record is harvested
+// (its events read and accumulated) when it is reused or on ofb_runtime_timing.
+struct StepRecord {
+  bool pending = false;
+  std::vector<cudaEvent_t> pool;
+  size_t next = 0;
+  cudaEvent_t start = nullptr;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> attn;
+  std::vector<CopyTiming> copies;
+  int streams = 0;
+};
+
+struct StepValues {
+  int32_t layers = 0, copies = 0, streams = 0;
+  float attn_total = 0, attn_max = 0, copy_sum = 0, copy_span = 0, step = 0;
+  double copy_bytes = 0;
+};
+
+constexpr int kTimingRing = 4;
+
+struct StepState {
+  bool active = false;
+  ofb_step_desc d{};
+  cudaStream_t cs = nullptr;
+  CUtensorMap map;
+  StepRecord* rec = nullptr;
+  std::vector<std::vector<int>> offl;
+  std::vector<size_t> next;
+  std::vector<cudaEvent_t> attn_done, fetch_done;
+  std::vector<char> waited_d2h;
+  int nstreams = 0;
+  bool any_fetch = false;
+  int next_layer = 0;
+};
+
 struct ofb_runtime {
+  StepState step;
   int device = 0;
   int max_streams = 16;
   std::vector<cudaStream_t> copy;
   cudaStream_t mig_h2d = nullptr, mig_d2h = nullptr;
   std::vector<cudaEvent_t> sync_events;  // timing-disabled, reused every step
   size_t next_sync = 0;
-  std::vector<cudaEvent_t> timing_events;
-  size_t next_timing = 0;
-  // last-step timing records
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> attn_t;
-  std::vector<CopyTiming> copy_t;
-  cudaEvent_t step_start = nullptr;
-  bool timed = false;
+  StepRecord ring[kTimingRing];
+  int ring_pos = 0;
+  StepValues last;
+  int32_t acc_steps = 0, acc_launches = 0;
+  double acc_attn_ms = 0, acc_copy_bytes = 0, acc_step_ms = 0;
   int streams_used = 0;
   // migration
-  bool pending_mig = false;
   cudaEvent_t mig_done_h2d = nullptr, mig_done_d2h = nullptr;
   cudaEvent_t mig_t0 = nullptr, mig_t1 = nullptr, mig_t2 = nullptr;
   bool mig_timed = false;
   double mig_h2d_bytes = 0, mig_d2h_bytes = 0;
-  std::vector<int> order_buf;
+  // host ranges still being written by the last eviction batch (D2H); fetches
+  // reading them wait for mig_done_d2h, everything else overlaps it
+  std::vector<std::pair<uint64_t, uint64_t>> pending_d2h;
 };
 
 namespace {
@@ -157,13 +193,63 @@ int next_sync_event(ofb_runtime* rt, cudaEvent_t* ev) {
   return 0;
 }
 
-int next_timing_event(ofb_runtime* rt, cudaEvent_t* ev) {
-  if (rt->next_timing == rt->timing_events.size()) {
+int next_timing_event(StepRecord* rec, cudaEvent_t* ev) {
+  if (rec->next == rec->pool.size()) {
     cudaEvent_t e;
     OFB_CUDA(cudaEventCreate(&e));
-    rt->timing_events.push_back(e);
+    rec->pool.push_back(e);
   }
-  *ev = rt->timing_events[rt->next_timing++];
+  *ev = rec->pool[rec->next++];
+  return 0;
+}
+
+// Read a finished record's events into rt->last and the accumulators.
+int harvest(ofb_runtime* rt, StepRecord* rec) {
+  if (!rec->pending) return 0;
+  rec->pending = false;
+  StepValues v;
+  v.streams = rec->streams;
+  float ms = 0;
+  for (auto& p : rec->attn) {
+    OFB_CUDA(cudaEventSynchronize(p.second));
+    OFB_CUDA(cudaEventElapsedTime(&ms, p.first, p.second));
+    v.attn_total += ms;
+    v.attn_max = std::max(v.attn_max, ms);
+  }
+  v.layers = static_cast<int32_t>(rec->attn.size());
+  if (!rec->attn.empty()) {
+    OFB_CUDA(cudaEventElapsedTime(&ms, rec->start, rec->attn.back().second));
+    v.step = ms;
+  }
+  float first = 1e30f, lastc = 0.f;
+  for (auto& c : rec->copies) {
+    OFB_CUDA(cudaEventSynchronize(c.stop));
+    OFB_CUDA(cudaEventElapsedTime(&ms, c.start, c.stop));
+    v.copy_sum += ms;
+    v.copy_bytes += c.bytes;
+    float a = 0, b = 0;
+    OFB_CUDA(cudaEventElapsedTime(&a, rec->start, c.start));
+    OFB_CUDA(cudaEventElapsedTime(&b, rec->start, c.stop));
+    first = std::min(first, a);
+    lastc = std::max(lastc, b);
+  }
+  v.copies = static_cast<int32_t>(rec->copies.size());
+  v.copy_span = rec->copies.empty() ? 0.f : lastc - first;
+  rt->last = v;
+  rt->acc_steps += 1;
+  rt->acc_launches += v.layers;
+  rt->acc_attn_ms += v.attn_total;
+  rt->acc_copy_bytes += v.copy_bytes;
+  rt->acc_step_ms += v.step;
+  return 0;
+}
+
+int harvest_all(ofb_runtime* rt) {
+  // oldest first: the record after ring_pos was written longest ago
+  for (int i = 0; i < kTimingRing; ++i) {
+    int rc = harvest(rt, &rt->ring[(rt->ring_pos + i) % kTimingRing]);
+    if (rc) return rc;
+  }
   return 0;
 }
 
@@ -295,61 +381,77 @@ int ofb_runtime_destroy(ofb_runtime* rt) {
   if (rt->mig_h2d) cudaStreamDestroy(rt->mig_h2d);
   if (rt->mig_d2h) cudaStreamDestroy(rt->mig_d2h);
   for (auto e : rt->sync_events) cudaEventDestroy(e);
-  for (auto e : rt->timing_events) cudaEventDestroy(e);
+  for (auto& rec : rt->ring)
+    for (auto e : rec.pool) cudaEventDestroy(e);
   for (cudaEvent_t e : {rt->mig_done_h2d, rt->mig_done_d2h, rt->mig_t0, rt->mig_t1, rt->mig_t2})
     if (e) cudaEventDestroy(e);
   delete rt;
   return 0;
 }
 
-int ofb_runtime_decode_step(ofb_runtime* rt, const ofb_step_desc* d, void* stream_) {
-  if (!rt || !d) return fail(-1, "ofb_runtime_decode_step: null argument");
+namespace {
+
+// One decode step in progress: begin() validates and issues the step-start
+// work, layers() enqueues fetches + compute for the next layers, end() checks
+// that every fetch was issued.  Splitting lets a caller interleave per-layer
+// work of its own (e.g. the TP o-projection + all-reduce) on the same stream.
+int step_begin(ofb_runtime* rt, const ofb_step_desc* d, cudaStream_t cs) {
+  StepState& st = rt->step;
+  if (st.active) return fail(-1, "a decode step is already in progress");
   int rc = check_shapes(d->batch, d->num_q_heads, d->num_kv_heads, d->head_dim);
   if (rc) return rc;
   const int L = d->num_layers, B = d->batch;
   if (L <= 0) return fail(-1, "num_layers must be > 0");
-  if (B == 0) return 0;
+  if (B <= 0) return fail(-1, "batch must be > 0");
   if (d->staging_slots < 1 || d->staging_slots > 8) return fail(-1, "staging_slots must be 1..8");
   if (!d->host_slabs || !d->staging_dst || !d->fetch_bytes)
     return fail(-1, "host transfer plan arrays are required");
-  cudaStream_t cs = static_cast<cudaStream_t>(stream_);
-  CUtensorMap map;
-  rc = get_kv_map(d->kv_pool, d->pool_blocks, d->num_kv_heads, &map);
+  rc = get_kv_map(d->kv_pool, d->pool_blocks, d->num_kv_heads, &st.map);
   if (rc) return rc;
+  st.d = *d;
+  st.cs = cs;
+  st.next_layer = 0;
 
   rt->next_sync = 0;
-  rt->next_timing = 0;
-  rt->attn_t.clear();
-  rt->copy_t.clear();
-  rt->timed = d->record_timing != 0;
+  st.rec = nullptr;
+  if (d->record_timing) {
+    st.rec = &rt->ring[rt->ring_pos];
+    rt->ring_pos = (rt->ring_pos + 1) % kTimingRing;
+    rc = harvest(rt, st.rec);  // step N-4: long finished in steady state
+    if (rc) return rc;
+    st.rec->next = 0;
+    st.rec->attn.clear();
+    st.rec->copies.clear();
+    st.rec->pending = true;
+  }
+  StepRecord* rec = st.rec;
 
   // Per-request offload lists (layer order) -> this step's fetch schedule.
-  std::vector<std::vector<int>> offl(B);
-  bool any_fetch = false;
+  st.offl.assign(B, {});
+  st.any_fetch = false;
   for (int l = 0; l < L; ++l)
     for (int b = 0; b < B; ++b)
       if (d->host_slabs[(size_t)l * B + b] != 0) {
-        offl[b].push_back(l);
-        any_fetch = true;
+        st.offl[b].push_back(l);
+        st.any_fetch = true;
       }
-  const int nstreams = any_fetch ? std::min(B, rt->max_streams) : 0;
-  rc = ensure_streams(rt, nstreams);
+  st.nstreams = st.any_fetch ? std::min(B, rt->max_streams) : 0;
+  rc = ensure_streams(rt, st.nstreams);
   if (rc) return rc;
-  rt->streams_used = nstreams;
+  rt->streams_used = st.nstreams;
+  if (rec) rec->streams = st.nstreams;
 
-  // Step start: a pending migration, then the append of every resident row.
-  // Copy streams start after it (staging from the previous step released).
-  // Offloaded rows get their token after their fetch lands (below), so a
-  // fetch moves exactly the b_r blocks the reference's blocks_to_fetch counts.
-  if (rt->pending_mig) {
-    OFB_CUDA(cudaStreamWaitEvent(cs, rt->mig_done_h2d, 0));
-    OFB_CUDA(cudaStreamWaitEvent(cs, rt->mig_done_d2h, 0));
-    rt->pending_mig = false;
-  }
-  if (rt->timed) {
-    rc = next_timing_event(rt, &rt->step_start);
+  // Step start: the append of every resident row.  Copy streams start after
+  // it (staging from the previous step released).  Offloaded rows get their
+  // token after their fetch lands (step_layers), so a fetch moves exactly the
+  // b_r blocks the reference's blocks_to_fetch counts.
+  if (!rt->pending_d2h.empty() && cudaEventQuery(rt->mig_done_d2h) == cudaSuccess)
+    rt->pending_d2h.clear();
+  st.waited_d2h.assign(st.nstreams, 0);
+  if (rec) {
+    rc = next_timing_event(rec, &rec->start);
     if (rc) return rc;
-    OFB_CUDA(cudaEventRecord(rt->step_start, cs));
+    OFB_CUDA(cudaEventRecord(rec->start, cs));
   }
   cudaError_t e = ofb::launch_kv_append(d->k_new, d->v_new, d->kv_pool, d->block_tables,
                                         d->max_blocks, d->positions, d->host_slabs_dev, L, B,
@@ -359,52 +461,73 @@ int ofb_runtime_decode_step(ofb_runtime* rt, const ofb_step_desc* d, void* strea
   rc = next_sync_event(rt, &ev_start);
   if (rc) return rc;
   OFB_CUDA(cudaEventRecord(ev_start, cs));
-  for (int s = 0; s < nstreams; ++s) OFB_CUDA(cudaStreamWaitEvent(rt->copy[s], ev_start, 0));
+  for (int s = 0; s < st.nstreams; ++s) OFB_CUDA(cudaStreamWaitEvent(rt->copy[s], ev_start, 0));
+  st.attn_done.assign(L, nullptr);
+  st.fetch_done.assign((size_t)L * B, nullptr);
+  st.next.assign(B, 0);
+  st.active = true;
+  return 0;
+}
 
-  std::vector<cudaEvent_t> attn_done(L, nullptr);
-  std::vector<cudaEvent_t> fetch_done((size_t)L * B, nullptr);
-  std::vector<size_t> next(B, 0);
+int step_layers(ofb_runtime* rt, int count) {
+  StepState& st = rt->step;
+  if (!st.active) return fail(-1, "no decode step in progress");
+  const ofb_step_desc* d = &st.d;
+  const int L = d->num_layers, B = d->batch;
   const int S = d->staging_slots;
   const size_t q_layer = (size_t)B * d->num_q_heads * ofb::kHeadDim * 2;
   const size_t bt_layer = (size_t)B * d->max_blocks;
-
-  for (int l = 0; l < L; ++l) {
+  cudaStream_t cs = st.cs;
+  StepRecord* rec = st.rec;
+  int rc = 0;
+  cudaError_t e;
+  const int stop = std::min(L, st.next_layer + std::max(count, 0));
+  for (int l = st.next_layer; l < stop; ++l) {
     // Fetches whose staging slot is (or will be, in stream order) free.
     for (int b = 0; b < B; ++b) {
-      while (next[b] < offl[b].size()) {
-        const size_t k = next[b];
-        const int dst_layer = offl[b][k];
-        cudaStream_t s = rt->copy[b % nstreams];
+      while (st.next[b] < st.offl[b].size()) {
+        const size_t k = st.next[b];
+        const int dst_layer = st.offl[b][k];
+        cudaStream_t s = rt->copy[b % st.nstreams];
         if (k >= (size_t)S) {
-          const int prev = offl[b][k - S];
+          const int prev = st.offl[b][k - S];
           if (prev >= l) break;  // that layer's attention is not enqueued yet
-          OFB_CUDA(cudaStreamWaitEvent(s, attn_done[prev], 0));
+          OFB_CUDA(cudaStreamWaitEvent(s, st.attn_done[prev], 0));
         }
         const size_t idx = (size_t)dst_layer * B + b;
+        if (!rt->pending_d2h.empty() && !st.waited_d2h[b % st.nstreams]) {
+          const uint64_t lo = d->host_slabs[idx], hi = lo + (uint64_t)d->fetch_bytes[b];
+          for (auto& iv : rt->pending_d2h)
+            if (lo < iv.second && iv.first < hi) {  // this slab is still being evicted
+              OFB_CUDA(cudaStreamWaitEvent(s, rt->mig_done_d2h, 0));
+              st.waited_d2h[b % st.nstreams] = 1;
+              break;
+            }
+        }
         cudaEvent_t t0 = nullptr, t1 = nullptr;
-        if (rt->timed) {
-          if ((rc = next_timing_event(rt, &t0)) || (rc = next_timing_event(rt, &t1))) return rc;
+        if (rec) {
+          if ((rc = next_timing_event(rec, &t0)) || (rc = next_timing_event(rec, &t1))) return rc;
           OFB_CUDA(cudaEventRecord(t0, s));
         }
         OFB_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(d->staging_dst[idx]),
                                  reinterpret_cast<const void*>(d->host_slabs[idx]),
                                  static_cast<size_t>(d->fetch_bytes[b]), cudaMemcpyHostToDevice, s));
-        if (rt->timed) {
+        if (rec) {
           OFB_CUDA(cudaEventRecord(t1, s));
-          rt->copy_t.push_back({t0, t1, static_cast<double>(d->fetch_bytes[b]), b % nstreams});
+          rec->copies.push_back({t0, t1, static_cast<double>(d->fetch_bytes[b]), b % st.nstreams});
         }
         cudaEvent_t done;
         if ((rc = next_sync_event(rt, &done))) return rc;
         OFB_CUDA(cudaEventRecord(done, s));
-        fetch_done[idx] = done;
-        ++next[b];
+        st.fetch_done[idx] = done;
+        ++st.next[b];
       }
     }
     // Layer l: stall until its own fetches landed (latency.py:185-187), write
     // the new token into the staged slabs (and their host slabs), then attend.
     bool layer_fetches = false;
     for (int b = 0; b < B; ++b) {
-      cudaEvent_t f = fetch_done[(size_t)l * B + b];
+      cudaEvent_t f = st.fetch_done[(size_t)l * B + b];
       if (f) {
         OFB_CUDA(cudaStreamWaitEvent(cs, f, 0));
         layer_fetches = true;
@@ -420,30 +543,71 @@ int ofb_runtime_decode_step(ofb_runtime* rt, const ofb_step_desc* d, void* strea
       if (e != cudaSuccess) return cuda_fail(e, "kv_append_kernel launch");
     }
     cudaEvent_t t0 = nullptr, t1 = nullptr;
-    if (rt->timed) {
-      if ((rc = next_timing_event(rt, &t0)) || (rc = next_timing_event(rt, &t1))) return rc;
+    if (rec) {
+      if ((rc = next_timing_event(rec, &t0)) || (rc = next_timing_event(rec, &t1))) return rc;
       OFB_CUDA(cudaEventRecord(t0, cs));
     }
     e = ofb::launch_decode_attention(
-        map, static_cast<const uint8_t*>(d->q) + l * q_layer,
+        st.map, static_cast<const uint8_t*>(d->q) + l * q_layer,
         static_cast<uint8_t*>(d->out) + l * q_layer, d->block_tables + l * bt_layer, d->max_blocks,
         d->seq_lens, d->workspace, static_cast<size_t>(d->workspace_bytes), B, d->num_q_heads,
         d->num_kv_heads, d->max_seq_len, d->scale, cs);
     if (e != cudaSuccess) return cuda_fail(e, "paged_gqa_decode_kernel launch");
-    if (rt->timed) {
+    if (rec) {
       OFB_CUDA(cudaEventRecord(t1, cs));
-      rt->attn_t.push_back({t0, t1});
+      rec->attn.push_back({t0, t1});
     }
-    if (any_fetch) {
+    if (st.any_fetch) {
       cudaEvent_t done;
       if ((rc = next_sync_event(rt, &done))) return rc;
       OFB_CUDA(cudaEventRecord(done, cs));
-      attn_done[l] = done;
+      st.attn_done[l] = done;
     }
   }
-  for (int b = 0; b < B; ++b)
-    if (next[b] != offl[b].size()) return fail(-1, "internal: fetch schedule did not drain");
+  st.next_layer = stop;
   return 0;
+}
+
+int step_end(ofb_runtime* rt) {
+  StepState& st = rt->step;
+  if (!st.active) return fail(-1, "no decode step in progress");
+  st.active = false;
+  if (st.next_layer != st.d.num_layers) return fail(-1, "decode step ended before its last layer");
+  for (int b = 0; b < st.d.batch; ++b)
+    if (st.next[b] != st.offl[b].size()) return fail(-1, "internal: fetch schedule did not drain");
+  return 0;
+}
+
+}  // namespace
+
+int ofb_runtime_decode_step(ofb_runtime* rt, const ofb_step_desc* d, void* stream_) {
+  if (!rt || !d) return fail(-1, "ofb_runtime_decode_step: null argument");
+  if (d->batch == 0) return 0;
+  int rc = step_begin(rt, d, static_cast<cudaStream_t>(stream_));
+  if (rc) return rc;
+  rc = step_layers(rt, d->num_layers);
+  if (rc) {
+    rt->step.active = false;
+    return rc;
+  }
+  return step_end(rt);
+}
+
+int ofb_runtime_step_begin(ofb_runtime* rt, const ofb_step_desc* d, void* stream_) {
+  if (!rt || !d) return fail(-1, "ofb_runtime_step_begin: null argument");
+  return step_begin(rt, d, static_cast<cudaStream_t>(stream_));
+}
+
+int ofb_runtime_step_layers(ofb_runtime* rt, int32_t count) {
+  if (!rt) return fail(-1, "ofb_runtime_step_layers: null runtime");
+  int rc = step_layers(rt, count);
+  if (rc) rt->step.active = false;
+  return rc;
+}
+
+int ofb_runtime_step_end(ofb_runtime* rt) {
+  if (!rt) return fail(-1, "ofb_runtime_step_end: null runtime");
+  return step_end(rt);
 }
 
 int ofb_runtime_migrate(ofb_runtime* rt, int32_t n, const uint64_t* dst, const uint64_t* src,
@@ -460,6 +624,9 @@ int ofb_runtime_migrate(ofb_runtime* rt, int32_t n, const uint64_t* dst, const u
   OFB_CUDA(cudaEventRecord(ev, cs));
   OFB_CUDA(cudaStreamWaitEvent(rt->mig_h2d, ev, 0));
   OFB_CUDA(cudaStreamWaitEvent(rt->mig_d2h, ev, 0));
+  // a restore may read a host slab the previous eviction batch is still writing
+  OFB_CUDA(cudaStreamWaitEvent(rt->mig_h2d, rt->mig_done_d2h, 0));
+  rt->pending_d2h.clear();
   rt->mig_timed = record_timing != 0;
   if (rt->mig_timed) OFB_CUDA(cudaEventRecord(rt->mig_t0, cs));
   rt->mig_h2d_bytes = rt->mig_d2h_bytes = 0;
@@ -468,7 +635,12 @@ int ofb_runtime_migrate(ofb_runtime* rt, int32_t n, const uint64_t* dst, const u
     cudaStream_t s;
     switch (kinds[i]) {
       case 0: kind = cudaMemcpyHostToDevice; s = rt->mig_h2d; rt->mig_h2d_bytes += bytes[i]; break;
-      case 1: kind = cudaMemcpyDeviceToHost; s = rt->mig_d2h; rt->mig_d2h_bytes += bytes[i]; break;
+      case 1:
+        kind = cudaMemcpyDeviceToHost;
+        s = rt->mig_d2h;
+        rt->mig_d2h_bytes += bytes[i];
+        if (bytes[i] > 0) rt->pending_d2h.emplace_back(dst[i], dst[i] + (uint64_t)bytes[i]);
+        break;
       case 2: kind = cudaMemcpyDeviceToDevice; s = rt->mig_h2d; break;
       default: return fail(-1, "ofb_runtime_migrate: bad kind");
     }
@@ -482,45 +654,46 @@ int ofb_runtime_migrate(ofb_runtime* rt, int32_t n, const uint64_t* dst, const u
     OFB_CUDA(cudaEventRecord(rt->mig_t1, rt->mig_h2d));
     OFB_CUDA(cudaEventRecord(rt->mig_t2, rt->mig_d2h));
   }
-  // Later compute (and the next step's fetches, via its start event) waits.
+  // Later compute (and, via its start event, the next step's fetches) waits for
+  // the restores only.  Evictions (D2H) overlap the next step's H2D fetches on
+  // the full-duplex link; only fetches of a slab still being written wait (see
+  // ofb_runtime_decode_step), and the caller recycles evicted HBM extents only
+  // once ofb_runtime_migration_pending() reports the batch done.
   OFB_CUDA(cudaStreamWaitEvent(cs, rt->mig_done_h2d, 0));
-  OFB_CUDA(cudaStreamWaitEvent(cs, rt->mig_done_d2h, 0));
-  rt->pending_mig = false;
+  return 0;
+}
+
+int ofb_runtime_migration_pending(ofb_runtime* rt, int32_t wait) {
+  if (!rt) return fail(-1, "ofb_runtime_migration_pending: null runtime");
+  if (rt->pending_d2h.empty()) return 0;
+  if (wait) OFB_CUDA(cudaEventSynchronize(rt->mig_done_d2h));
+  cudaError_t q = cudaEventQuery(rt->mig_done_d2h);
+  if (q == cudaErrorNotReady) return 1;
+  if (q != cudaSuccess) return cuda_fail(q, "cudaEventQuery(mig_done_d2h)");
+  rt->pending_d2h.clear();
   return 0;
 }
 
 int ofb_runtime_timing(ofb_runtime* rt, ofb_step_timing* out) {
   if (!rt || !out) return fail(-1, "ofb_runtime_timing: null argument");
   std::memset(out, 0, sizeof(*out));
-  out->copy_streams = rt->streams_used;
-  if (rt->timed) {
-    float ms = 0;
-    for (auto& p : rt->attn_t) {
-      OFB_CUDA(cudaEventSynchronize(p.second));
-      OFB_CUDA(cudaEventElapsedTime(&ms, p.first, p.second));
-      out->attn_ms_total += ms;
-      out->attn_ms_max = std::max(out->attn_ms_max, ms);
-    }
-    out->layers = static_cast<int32_t>(rt->attn_t.size());
-    if (!rt->attn_t.empty()) {
-      OFB_CUDA(cudaEventElapsedTime(&ms, rt->step_start, rt->attn_t.back().second));
-      out->step_ms = ms;
-    }
-    float first = 1e30f, last = 0.f;
-    for (auto& c : rt->copy_t) {
-      OFB_CUDA(cudaEventSynchronize(c.stop));
-      OFB_CUDA(cudaEventElapsedTime(&ms, c.start, c.stop));
-      out->copy_ms_sum += ms;
-      out->copy_bytes += c.bytes;
-      float a = 0, b = 0;
-      OFB_CUDA(cudaEventElapsedTime(&a, rt->step_start, c.start));
-      OFB_CUDA(cudaEventElapsedTime(&b, rt->step_start, c.stop));
-      first = std::min(first, a);
-      last = std::max(last, b);
-    }
-    out->copies = static_cast<int32_t>(rt->copy_t.size());
-    out->copy_span_ms = rt->copy_t.empty() ? 0.f : last - first;
-  }
+  int rc = harvest_all(rt);
+  if (rc) return rc;
+  const StepValues& v = rt->last;
+  out->copy_streams = v.streams;
+  out->layers = v.layers;
+  out->attn_ms_total = v.attn_total;
+  out->attn_ms_max = v.attn_max;
+  out->copies = v.copies;
+  out->copy_ms_sum = v.copy_sum;
+  out->copy_bytes = v.copy_bytes;
+  out->copy_span_ms = v.copy_span;
+  out->step_ms = v.step;
+  out->acc_steps = rt->acc_steps;
+  out->acc_attn_launches = rt->acc_launches;
+  out->acc_attn_ms = rt->acc_attn_ms;
+  out->acc_copy_bytes = rt->acc_copy_bytes;
+  out->acc_step_ms = rt->acc_step_ms;
   if (rt->mig_timed) {
     float a = 0, b = 0;
     OFB_CUDA(cudaEventSynchronize(rt->mig_t1));
@@ -531,6 +704,15 @@ int ofb_runtime_timing(ofb_runtime* rt, ofb_step_timing* out) {
     out->mig_h2d_bytes = rt->mig_h2d_bytes;
     out->mig_d2h_bytes = rt->mig_d2h_bytes;
   }
+  return 0;
+}
+
+int ofb_runtime_timing_reset(ofb_runtime* rt) {
+  if (!rt) return fail(-1, "ofb_runtime_timing_reset: null runtime");
+  int rc = harvest_all(rt);
+  if (rc) return rc;
+  rt->acc_steps = rt->acc_launches = 0;
+  rt->acc_attn_ms = rt->acc_copy_bytes = rt->acc_step_ms = 0;
   return 0;
 }
 

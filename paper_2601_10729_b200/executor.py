@@ -23,6 +23,7 @@ KV values are synthetic (seeded N(0,1) bf16): there is no model checkpoint.
 from __future__ import annotations
 
 import math
+from collections import deque
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -105,6 +106,10 @@ class B200Executor:
         self.migrated = {"h2d_bytes": 0, "d2h_bytes": 0, "moves": 0}
         self._ws = None
         self._mig_start = None        # event before the last un-stepped migration
+        self._deferred: list = []     # evicted extents awaiting their D2H
+        self._inflight: deque = deque()   # (done event, resources) of un-synced steps
+        self._pin_ring: list = []         # pinned [positions | lens] staging per in-flight step
+        self._step_dev = None             # device [positions | lens]
 
     # ------------------------------------------------------------ sizing
     @classmethod
@@ -144,7 +149,27 @@ class B200Executor:
                              np.array([src.data_ptr()], dtype=np.uint64),
                              np.array([used * self.shape.block_bytes], dtype=np.int64),
                              np.array([1], dtype=np.int32))
-        torch.cuda.current_stream().synchronize()  # src is a temporary
+        self.runtime.migration_pending(wait=True)  # src is a temporary
+
+    # ------------------------------------------------------------ HBM extents
+    def _reclaim(self, wait: bool) -> None:
+        """Recycle extents evicted by earlier migrations once their D2H landed."""
+        if self._deferred and not self.runtime.migration_pending(wait=wait):
+            for start, cap in self._deferred:
+                self.pool.alloc.release(start, cap)
+            self._deferred.clear()
+
+    def _alloc_dev(self, n: int) -> int:
+        from .kvpool import PoolExhausted
+
+        self._reclaim(wait=False)
+        try:
+            return self.pool.alloc.alloc(n)
+        except PoolExhausted:
+            if not self._deferred:
+                raise
+            self._reclaim(wait=True)
+            return self.pool.alloc.alloc(n)
 
     # ------------------------------------------------------------ table sync (K4)
     def _ensure(self, req: RequestState) -> _RequestSlabs:
@@ -173,7 +198,7 @@ class B200Executor:
             for layer, loc in enumerate(locs):
                 on_dev = st.dev[layer] is not None
                 if loc in _DEVICE_LOCS and not on_dev:
-                    start = self.pool.alloc.alloc(st.capacity)
+                    start = self._alloc_dev(st.capacity)
                     st.dev[layer] = start
                     if fresh or st.host[layer] is None:
                         self._prefill_device(rid, layer, start, used)
@@ -199,12 +224,9 @@ class B200Executor:
             for _d, _s, n, kind in moves:
                 self.migrated["h2d_bytes" if kind == 0 else "d2h_bytes"] += int(n)
             self.migrated["moves"] += len(moves)
-        # Evicted extents are freed only after this batch was enqueued, so no
-        # restore above can alias them; later reuse is ordered behind the
-        # migration because the compute stream (and the next step's copy
-        # streams) wait for it.
-        for start, cap in evicted:
-            self.pool.alloc.release(start, cap)
+        # Evicted extents are recycled only once their D2H has landed (the
+        # eviction overlaps the next step; see ofb_runtime_migrate).
+        self._deferred.extend(evicted)
         self.layout_version += 1
 
     def install(self, batch: list[RequestState], placement: PlacementMatrix) -> None:
@@ -246,7 +268,7 @@ class B200Executor:
             offloaded = [l for l in range(L) if st.dev[l] is None]
             if offloaded and len(st.staging) < self.staging_slots:
                 while len(st.staging) < self.staging_slots:
-                    st.staging.append(self.pool.alloc.alloc(st.capacity))
+                    st.staging.append(self._alloc_dev(st.capacity))
             for l in range(L):
                 if st.dev[l] is not None:
                     tables[l, b, : st.capacity] = st.dev[l] + ramp
@@ -298,8 +320,20 @@ class B200Executor:
         if inputs is None:
             inputs = self.synthetic_inputs(B)
         out = torch.empty_like(inputs["q"])
-        pos_dev = torch.from_numpy(positions).to(self.device, non_blocking=False)
-        lens_dev = torch.from_numpy(lens.astype(np.int32)).to(self.device, non_blocking=False)
+        # per-step scalars: pinned ring slot -> one async H2D into a device buffer
+        # (stream-ordered, so the previous step has consumed it)
+        slot = self.steps % 4
+        if len(self._pin_ring) < 4 or self._pin_ring[slot].numel() < 2 * B:
+            self._pin_ring = [torch.empty(2 * max(B, 64), dtype=torch.int32).pin_memory()
+                              for _ in range(4)]
+            self._step_dev = torch.empty(2 * max(B, 64), dtype=torch.int32, device=self.device)
+        pin = self._pin_ring[slot]
+        pin_np = pin.numpy()
+        pin_np[:B] = positions
+        pin_np[B:2 * B] = lens
+        step_dev = self._step_dev[: 2 * B]
+        step_dev.copy_(pin[: 2 * B], non_blocking=True)
+        pos_dev, lens_dev = step_dev[:B], step_dev[B:]
         ws = self._workspace(B, max_seq)
         d = _native.StepDesc()
         d.num_layers, d.batch = L, B
@@ -323,8 +357,13 @@ class B200Executor:
         return d, keep
 
     def decode_step(self, batch: list[RequestState], placement: PlacementMatrix | None = None,
-                    inputs: dict | None = None) -> float:
-        """Run one decode step on the GPU; returns its device time in ms."""
+                    inputs: dict | None = None, sync: bool = True) -> float | None:
+        """Run one decode step on the GPU.
+
+        ``sync=True`` waits for it and returns its device time in ms (the engine
+        seam).  ``sync=False`` only enqueues (up to 4 steps in flight) so the host
+        prepares the next step while the GPU runs this one; call ``drain()``.
+        """
         if placement is not None:
             for req, row in zip(batch, placement.rows):
                 st = self.slabs.get(req.id)
@@ -340,13 +379,24 @@ class B200Executor:
             t0.record(stream)
         self.runtime.decode_step(desc, stream)
         t1.record(stream)
-        t1.synchronize()
         self.steps += 1
         self.last_inputs, self.last_output = keep[0], keep[1]
         self.last_positions = np.array([r.total_tokens for r in batch], dtype=np.int32)
+        self._inflight.append((t1, keep))
+        if not sync:
+            while len(self._inflight) > 3:
+                self._inflight.popleft()[0].synchronize()
+            return None
+        t1.synchronize()
+        self._inflight.clear()
         if self.record_timing:
             self.last_timing = self.runtime.timing()
         return t0.elapsed_time(t1)
+
+    def drain(self) -> None:
+        """Wait for every enqueued step."""
+        while self._inflight:
+            self._inflight.popleft()[0].synchronize()
 
     # ------------------------------------------------------------ inspection
     def slab_bits(self, rid: int, layer: int, blocks: int) -> np.ndarray:

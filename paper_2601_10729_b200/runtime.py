@@ -33,6 +33,17 @@ class StepRuntime:
         rc = self.lib.ofb_runtime_decode_step(self.handle, ctypes.byref(desc), s.cuda_stream)
         _native.check(rc, "ofb_runtime_decode_step")
 
+    def step_begin(self, desc: _native.StepDesc, stream=None) -> None:
+        s = stream if stream is not None else torch.cuda.current_stream()
+        rc = self.lib.ofb_runtime_step_begin(self.handle, ctypes.byref(desc), s.cuda_stream)
+        _native.check(rc, "ofb_runtime_step_begin")
+
+    def step_layers(self, count: int) -> None:
+        _native.check(self.lib.ofb_runtime_step_layers(self.handle, count), "ofb_runtime_step_layers")
+
+    def step_end(self) -> None:
+        _native.check(self.lib.ofb_runtime_step_end(self.handle), "ofb_runtime_step_end")
+
     def migrate(self, dst: np.ndarray, src: np.ndarray, nbytes: np.ndarray, kinds: np.ndarray,
                 record_timing: bool = False, stream=None) -> None:
         n = len(dst)
@@ -47,10 +58,19 @@ class StepRuntime:
                                           _ptr(kinds), int(record_timing), s.cuda_stream)
         _native.check(rc, "ofb_runtime_migrate")
 
+    def migration_pending(self, wait: bool = False) -> bool:
+        rc = self.lib.ofb_runtime_migration_pending(self.handle, int(wait))
+        if rc < 0 or rc > 1:
+            _native.check(rc, "ofb_runtime_migration_pending")
+        return rc == 1
+
     def timing(self) -> dict:
         t = _native.StepTiming()
         _native.check(self.lib.ofb_runtime_timing(self.handle, ctypes.byref(t)), "ofb_runtime_timing")
         return {name: getattr(t, name) for name, _ in _native.StepTiming._fields_}
+
+    def timing_reset(self) -> None:
+        _native.check(self.lib.ofb_runtime_timing_reset(self.handle), "ofb_runtime_timing_reset")
 
     def close(self) -> None:
         if self.handle:
