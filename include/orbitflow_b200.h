@@ -40,6 +40,10 @@ extern "C" {
 /* ---- library ----------------------------------------------------------- */
 OFB_API const char* ofb_version(void);
 OFB_API const char* ofb_last_error(void);
+/* K1 work decomposition for later launches: 0 = persistent stream-K, 1 = fixed
+ * splits + last-CTA combine, 2 = auto (default: stream-K unless few (request,
+ * kv head) pairs span the whole grid).  Returns the previous variant. */
+OFB_API int ofb_set_attention_kernel(int32_t variant);
 /* SM count and resident attention CTAs per SM on the current device. */
 OFB_API int ofb_device_info(int32_t* num_sms, int32_t* attn_ctas_per_sm);
 

@@ -18,7 +18,9 @@
 //   * the 4 warp states merge through shared memory; multi-split requests
 //     write (O, lse) partials and the last CTA of a (request, kv head) to
 //     arrive (atomic ticket) combines them - no second launch.
-#include "common.cuh"
+#include "attn_tile.cuh"
+#include <cstdlib>
+#include <cstring>
 
 namespace ofb {
 
@@ -27,7 +29,6 @@ constexpr int kAttnThreads = (kConsumerWarps + 1) * 32;
 constexpr int kStages = 8;
 constexpr int kMaxSplits = 256;
 constexpr int kMaxBlocksPerSplit = 256;
-constexpr int kMaxGroup = 16;
 // Split tickets live in a fixed region at the start of the workspace, sized for
 // the largest (request x kv head) grid, so partials of a previous launch with
 // a different batch can never alias a counter.
@@ -61,12 +62,6 @@ static_assert(kMaxGroup * kMaxSplits * sizeof(float) + kMaxGroup * 2 * sizeof(fl
 constexpr size_t kAttnSmemBytes = 1024 /*align slack*/ + kRingBytes +
                                   2 * kStages * sizeof(uint64_t) +
                                   kMaxBlocksPerSplit * sizeof(int32_t) + 16;
-
-__device__ __forceinline__ uint32_t tile_addr(uint32_t base, int row, int chunk) {
-  // Tile = two 128B-swizzled halves of [32 rows][64 bf16]; `chunk` is the 16 B
-  // column unit (0..15) of the logical 256 B row.
-  return base + ((chunk >> 3) << 12) + (row << 7) + ((((chunk & 7) ^ (row & 7))) << 4);
-}
 
 __global__ void __launch_bounds__(kAttnThreads, 2)
 paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnArgs a) {
@@ -405,7 +400,49 @@ static AttnPlan plan_splits(int batch, int hkv, int max_seq_len) {
   return p;
 }
 
+size_t attention_stream_workspace_bytes(int batch, int hq, int hkv, int max_seq_len);
+cudaError_t launch_decode_attention_stream(const CUtensorMap& map, const void* q, void* out,
+                                           const int32_t* block_tables, int max_blocks,
+                                           const int32_t* seq_lens, void* workspace,
+                                           size_t workspace_bytes, int batch, int hq, int hkv,
+                                           int max_seq_len, float scale, cudaStream_t stream);
+
+// K1 work decomposition: "stream" (persistent stream-K, default) or "split"
+// (fixed splits + last-CTA combine); OFB_K1=split selects the latter.
+bool stream_preferred(int batch, int hkv, int max_seq_len);
+
+// 0 = stream-K, 1 = fixed splits, 2 = auto (default; OFB_K1=stream|split pins one)
+static int g_k1_variant = -1;
+
+static int k1_variant() {
+  if (g_k1_variant < 0) {
+    const char* v = std::getenv("OFB_K1");
+    g_k1_variant = !v ? 2 : std::strcmp(v, "split") == 0 ? 1 : std::strcmp(v, "stream") == 0 ? 0 : 2;
+  }
+  return g_k1_variant;
+}
+
+static bool use_split_kernel(int batch, int hkv, int max_seq_len) {
+  const int v = k1_variant();
+  if (v == 2) return !stream_preferred(batch, hkv, max_seq_len);
+  return v == 1;
+}
+
+int set_attention_variant(int variant) {
+  const int prev = k1_variant();
+  if (variant >= 0 && variant <= 2) g_k1_variant = variant;
+  return prev;
+}
+
+static size_t split_workspace_bytes(int batch, int hq, int hkv, int max_seq_len);
+
 size_t attention_workspace_bytes(int batch, int hq, int hkv, int max_seq_len) {
+  const size_t a = split_workspace_bytes(batch, hq, hkv, max_seq_len);
+  const size_t b = attention_stream_workspace_bytes(batch, hq, hkv, max_seq_len);
+  return a > b ? a : b;
+}
+
+static size_t split_workspace_bytes(int batch, int hq, int hkv, int max_seq_len) {
   const int nblk = (max_seq_len + kBlockTokens - 1) / kBlockTokens;
   int splits = nblk < 1 ? 1 : nblk;
   if (splits > kMaxSplits) splits = kMaxSplits;
@@ -421,11 +458,15 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
                                     size_t workspace_bytes, int batch, int hq, int hkv,
                                     int max_seq_len, float scale, cudaStream_t stream) {
   if (batch <= 0) return cudaSuccess;
+  if (!use_split_kernel(batch, hkv, max_seq_len))
+    return launch_decode_attention_stream(map, q, out, block_tables, max_blocks, seq_lens,
+                                          workspace, workspace_bytes, batch, hq, hkv, max_seq_len,
+                                          scale, stream);
   if (hkv <= 0 || hq % hkv != 0 || hq / hkv > kMaxGroup) return cudaErrorInvalidValue;
   if ((size_t)batch * hkv * sizeof(int32_t) > kCounterRegionBytes) return cudaErrorInvalidValue;
   cudaError_t e = attn_init_once();
   if (e != cudaSuccess) return e;
-  if (workspace_bytes < attention_workspace_bytes(batch, hq, hkv, max_seq_len))
+  if (workspace_bytes < split_workspace_bytes(batch, hq, hkv, max_seq_len))
     return cudaErrorInvalidValue;
   const AttnPlan plan = plan_splits(batch, hkv, max_seq_len);
   const int nblk = (max_seq_len + kBlockTokens - 1) / kBlockTokens;

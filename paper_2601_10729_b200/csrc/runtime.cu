@@ -31,6 +31,7 @@ cudaError_t launch_kv_append(const void* k_new, const void* v_new, void* pool,
                              int num_layers, int batch, int hkv, int mode,
                              cudaStream_t stream);
 int attention_occupancy();
+int set_attention_variant(int variant);
 }  // namespace ofb
 
 namespace {
@@ -269,6 +270,11 @@ extern "C" {
 const char* ofb_version(void) { return "orbitflow-b200 0.1 sm_100a"; }
 
 const char* ofb_last_error(void) { return g_err.c_str(); }
+
+int ofb_set_attention_kernel(int32_t variant) {
+  if (variant < 0 || variant > 2) return fail(-1, "variant must be 0 (stream-K), 1 (split) or 2 (auto)");
+  return ofb::set_attention_variant(variant);
+}
 
 int ofb_device_info(int32_t* num_sms, int32_t* attn_ctas_per_sm) {
   int dev = 0;

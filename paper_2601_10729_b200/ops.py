@@ -121,3 +121,13 @@ def device_info() -> tuple[int, int]:
     occ = _native.c_i32()
     _native.check(lib.ofb_device_info(ctypes.byref(sms), ctypes.byref(occ)), "ofb_device_info")
     return sms.value, occ.value
+
+
+def set_attention_kernel(variant: str) -> str:
+    """Select K1's work decomposition: "stream" (persistent stream-K), "split"
+    (fixed splits + last-CTA combine) or "auto" (default).  Returns the previous one."""
+    names = {"stream": 0, "split": 1, "auto": 2}
+    prev = _native.load().ofb_set_attention_kernel(names[variant])
+    if prev < 0:
+        _native.check(prev, "ofb_set_attention_kernel")
+    return {v: k for k, v in names.items()}[prev]

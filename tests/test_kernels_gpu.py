@@ -17,6 +17,16 @@ pytestmark = pytest.mark.gpu
 RTOL, ATOL = 2e-2, 1e-2
 
 
+@pytest.fixture(params=["stream", "split"], autouse=True)
+def k1_variant(request):
+    """Every K1 parity test runs under both work decompositions."""
+    from paper_2601_10729_b200 import ops
+
+    prev = ops.set_attention_kernel(request.param)
+    yield request.param
+    ops.set_attention_kernel(prev)
+
+
 def _run_gpu(case, max_seq_len=None):
     from paper_2601_10729_b200 import ops
 
@@ -124,4 +134,29 @@ def test_garbage_past_sequence_end_is_ignored():
     case["pool"] = pool
     got = _run_gpu(case)
     assert not np.isnan(got).any()
+    np.testing.assert_allclose(got, _run_oracle(case), rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_ragged_batch_with_empty_and_tiny_requests(seed):
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(0, 3000, size=37)
+    lens[[3, 11, 20]] = 0
+    lens[[5, 6]] = 1
+    lens[7] = 16
+    lens[8] = 17
+    case = make_case(lens.tolist(), 8, 2, seed=seed)
+    got = _run_gpu(case, max_seq_len=int(lens.max()))
+    want = _run_oracle(case)
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+
+
+def test_one_pair_spans_every_cta():
+    case = make_case([100_000], 4, 1, seed=4)     # 6250 tiles over the whole grid
+    np.testing.assert_allclose(_run_gpu(case), _run_oracle(case), rtol=RTOL, atol=ATOL)
+
+
+def test_max_seq_len_overestimate_and_tiny_work():
+    case = make_case([5, 3], 8, 2, seed=6, max_blocks=4096)   # W = 2 tiles, grid sized for 64K
+    got = _run_gpu(case, max_seq_len=65536)
     np.testing.assert_allclose(got, _run_oracle(case), rtol=RTOL, atol=ATOL)

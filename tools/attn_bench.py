@@ -12,8 +12,10 @@ ap.add_argument("--hkv", type=int, default=8)
 ap.add_argument("--seq", type=int, default=32768)
 ap.add_argument("--layers", type=int, default=8, help="distinct layer pools rotated (defeats L2)")
 ap.add_argument("--iters", type=int, default=20)
+ap.add_argument("--variant", default="auto", choices=["stream", "split", "auto"])
 a = ap.parse_args()
 dev = torch.device("cuda:0")
+ops.set_attention_kernel(a.variant)
 nblk = (a.seq + 15) // 16
 pools = [torch.empty((a.batch * nblk, a.hkv, 2, 16, 128), dtype=torch.bfloat16, device=dev).normal_() for _ in range(a.layers)]
 bt = torch.arange(a.batch * nblk, dtype=torch.int32, device=dev).reshape(a.batch, nblk)
