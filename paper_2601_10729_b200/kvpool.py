@@ -68,20 +68,19 @@ class ExtentAllocator:
             return
         if start < 0 or start + n > self.capacity:
             raise ValueError("extent outside the pool")
-        self.in_use -= n
         i = bisect.bisect_left(self._starts, start)
-        # merge with the following free run
-        if i < len(self._starts) and self._starts[i] == start + n:
-            nxt = self._starts.pop(i)
+        nxt = self._starts[i] if i < len(self._starts) else None
+        prev = self._starts[i - 1] if i > 0 else None
+        if (nxt is not None and nxt < start + n) or (
+                prev is not None and prev + self._lengths[prev] > start):
+            raise ValueError("double free (extent overlaps a free run)")
+        self.in_use -= n
+        if nxt is not None and nxt == start + n:          # merge with the following run
+            self._starts.pop(i)
             n += self._lengths.pop(nxt)
-        # merge with the preceding free run
-        if i > 0:
-            prev = self._starts[i - 1]
-            if prev + self._lengths[prev] == start:
-                self._lengths[prev] += n
-                return
-            if prev + self._lengths[prev] > start:
-                raise ValueError("double free")
+        if prev is not None and prev + self._lengths[prev] == start:   # and the preceding one
+            self._lengths[prev] += n
+            return
         self._insert(start, n)
 
     @property
