@@ -186,6 +186,39 @@ OFB_API int ofb_runtime_migration_pending(ofb_runtime* rt, int32_t wait);
 OFB_API int ofb_runtime_timing(ofb_runtime* rt, ofb_step_timing* out);
 OFB_API int ofb_runtime_timing_reset(ofb_runtime* rt);
 
+/* ---- native exact placement solver (host code, no GPU needed) ---------- */
+/* Bit-exact restatement of kvsim solve / solve_capacity_only
+ * (kvsim/planner.py:437-560), multithreaded.  Balances follow the reference's
+ * two seeds: `live_balance` / `parked_balance` = snapshot.get(id,
+ * deposit_balance) (first-step pre-rejection, planner.py:470-483) and
+ * `forecast_live` / `forecast_parked` = the forecast's seed
+ * (planner.py:160-163). */
+typedef struct ofb_plan_problem {
+  int32_t num_layers, batch, num_paused, block_size;
+  double compute_base_ms, compute_per_token_ms, bandwidth_blocks_per_ms;
+  int64_t gpu_block_budget;
+  double tbt_ms, violation_cap;
+  int32_t window_min, window_max, current_step;
+  int32_t mode;                   /* 0 = solve, 1 = solve_capacity_only */
+  int32_t threads;
+  const int64_t* total_tokens;    /* [batch] */
+  const int64_t* blocks;          /* [batch] blocks per layer */
+  const double* live_balance;     /* [batch] */
+  const double* parked_balance;   /* [num_paused] */
+  const double* forecast_live;    /* [batch] */
+  const double* forecast_parked;  /* [num_paused] */
+  int32_t* strides_out;           /* [batch] chosen stride, -1 = resident */
+} ofb_plan_problem;
+
+typedef struct ofb_plan_result {
+  int32_t status;         /* 0 plan, 1 no placement fits the budget, 2 cap unsatisfiable */
+  int32_t decode_window, expiry_step;
+  int64_t candidates_feasible, candidates_priced, candidates_ranked;
+} ofb_plan_result;
+
+OFB_API int ofb_plan_solve(const ofb_plan_problem* problem, ofb_plan_result* result);
+OFB_API const char* ofb_plan_last_error(void);
+
 /* Host-link probe: best-of-reps pinned cudaMemcpyAsync in each direction. */
 OFB_API int ofb_link_probe(void* host, void* dev, int64_t bytes, int32_t reps, double* h2d_gbs,
                    double* d2h_gbs);

@@ -55,6 +55,30 @@ class StepTiming(ctypes.Structure):
     ]
 
 
+class PlanProblem(ctypes.Structure):
+    """Mirror of ``ofb_plan_problem``."""
+
+    _fields_ = [
+        ("num_layers", c_i32), ("batch", c_i32), ("num_paused", c_i32), ("block_size", c_i32),
+        ("compute_base_ms", c_f64), ("compute_per_token_ms", c_f64),
+        ("bandwidth_blocks_per_ms", c_f64), ("gpu_block_budget", c_i64),
+        ("tbt_ms", c_f64), ("violation_cap", c_f64),
+        ("window_min", c_i32), ("window_max", c_i32), ("current_step", c_i32),
+        ("mode", c_i32), ("threads", c_i32),
+        ("total_tokens", c_vp), ("blocks", c_vp), ("live_balance", c_vp),
+        ("parked_balance", c_vp), ("forecast_live", c_vp), ("forecast_parked", c_vp),
+        ("strides_out", c_vp),
+    ]
+
+
+class PlanResult(ctypes.Structure):
+    """Mirror of ``ofb_plan_result``."""
+
+    _fields_ = [("status", c_i32), ("decode_window", c_i32), ("expiry_step", c_i32),
+                ("candidates_feasible", c_i64), ("candidates_priced", c_i64),
+                ("candidates_ranked", c_i64)]
+
+
 # name -> (restype, argtypes); exactly the symbols include/orbitflow_b200.h declares
 SIGNATURES = {
     "ofb_version": (ctypes.c_char_p, []),
@@ -78,6 +102,8 @@ SIGNATURES = {
     "ofb_runtime_timing": (ctypes.c_int, [c_vp, ctypes.POINTER(StepTiming)]),
     "ofb_runtime_migration_pending": (ctypes.c_int, [c_vp, c_i32]),
     "ofb_runtime_timing_reset": (ctypes.c_int, [c_vp]),
+    "ofb_plan_solve": (ctypes.c_int, [ctypes.POINTER(PlanProblem), ctypes.POINTER(PlanResult)]),
+    "ofb_plan_last_error": (ctypes.c_char_p, []),
     "ofb_link_probe": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, ctypes.POINTER(c_f64),
                                       ctypes.POINTER(c_f64)]),
 }

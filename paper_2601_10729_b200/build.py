@@ -19,7 +19,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_lib"
 LIB_NAME = "liborbitflow_b200.so"
-SOURCES = ["decode_attention.cu", "decode_attention_stream.cu", "kv_append.cu", "runtime.cu"]
+SOURCES = ["decode_attention.cu", "decode_attention_stream.cu", "kv_append.cu", "runtime.cu",
+           "planner.cpp"]
 
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [
@@ -63,12 +64,14 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
         obj = OUT_DIR / (Path(src).stem + ".o")
         cmd = [nvcc(), *ARCH_FLAGS, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(CSRC / src), "-o", str(obj)]
         cmd.extend(["-Xcompiler", "-fvisibility=hidden"])
+        if src.endswith(".cpp"):   # host-only planner: no FMA contraction (bit-exact plans)
+            cmd.extend(["-x", "c++", "-Xcompiler", "-ffp-contract=off", "-Xcompiler", "-pthread"])
         if ptxas_verbose:
             cmd.extend(["-Xptxas", "-v"])
         _run(cmd, verbose or ptxas_verbose)
         objs.append(str(obj))
     tmp = target.with_suffix(".so.tmp")
-    _run([nvcc(), *ARCH_FLAGS, "-shared", "-cudart", "shared", "-o", str(tmp), *objs, "-lcuda"
+    _run([nvcc(), *ARCH_FLAGS, "-shared", "-cudart", "shared", "-Xcompiler", "-pthread", "-o", str(tmp), *objs, "-lcuda"
           if _has_libcuda() else "-L/usr/local/cuda/lib64/stubs"], verbose)
     os.replace(tmp, target)
     return target

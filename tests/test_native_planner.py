@@ -1,0 +1,88 @@
+"""The native exact solver (ofb_plan_solve) returns the same plans as the numpy
+restatement (itself pinned to the reference by tests/test_golden.py and the
+reference suite) on random instances, including batches past the reference's
+tractable range.  CPU-only: the planner is host code."""
+
+import random
+import time
+
+import pytest
+
+from paper_2601_10729_b200 import planner
+from paper_2601_10729_b200.core import PlacementMatrix, RequestState, SloConfig, SystemProfile
+from paper_2601_10729_b200.latency import batch_decode_latency_fast
+
+
+def _plan_sig(p):
+    if isinstance(p, planner.Infeasible):
+        return ("infeasible", p.reason)
+    return (p.placement.rows, p.decode_window, p.expiry_step,
+            p.predicted_latency.total_latency_ms.hex())
+
+
+def _instance(rng, L, B):
+    batch = [RequestState(id=r, arrival_time_ms=float(rng.randint(0, 3)),
+                          prompt_tokens=rng.randint(10, 900), target_output_tokens=400)
+             for r in range(B)]
+    for r in batch:
+        r.generated_tokens = rng.randint(0, 20)
+        r.deposit_balance = rng.randint(0, 2)
+        r.sync_blocks()
+    total = sum(r.blocks_per_layer for r in batch) * L
+    prof = SystemProfile(L, rng.choice([0.1, 0.3, 1.0]), rng.choice([0.0, 0.0003]),
+                         rng.choice([3.0, 20.0, 80.0]),
+                         max(max(r.blocks_per_layer for r in batch) + 2,
+                             int(total * rng.uniform(0.3, 1.1))), 16)
+    base = batch_decode_latency_fast(PlacementMatrix.all_resident([r.id for r in batch], L),
+                                     batch, prof).total_latency_ms
+    slo = SloConfig(base * rng.choice([1.0, 1.3, 2.0, 5.0]), base * 2,
+                    violation_cap=rng.choice([0.5, 1.0, 2.0]), window_min=rng.randint(1, 4),
+                    window_max=rng.randint(4, 12))
+    paused = tuple(RequestState(id=50 + j, arrival_time_ms=0.0, prompt_tokens=rng.randint(10, 200),
+                                target_output_tokens=100) for j in range(rng.choice([0, 1])))
+    snap = None if rng.random() < 0.5 else {r.id: rng.uniform(0, 2) for r in [*batch, *paused]}
+    return batch, prof, slo, paused, snap
+
+
+def _both(fn):
+    old = planner.SOLVER
+    try:
+        planner.SOLVER = "native"
+        a = fn()
+        planner.SOLVER = "python"
+        b = fn()
+    finally:
+        planner.SOLVER = old
+    return a, b
+
+
+@pytest.mark.parametrize("L,B,count", [(4, 4, 60), (9, 3, 60), (12, 3, 40), (32, 3, 25), (32, 4, 6)])
+def test_native_matches_numpy(L, B, count):
+    rng = random.Random(L * 100 + B)
+    for _ in range(count):
+        batch, prof, slo, paused, snap = _instance(rng, L, B)
+        step = rng.randint(1, 30)
+        a, b = _both(lambda: planner.solve(batch, prof, slo, step, paused=paused,
+                                           deposit_snapshot=snap))
+        assert _plan_sig(a) == _plan_sig(b)
+        a, b = _both(lambda: planner.solve_capacity_only(batch, prof, slo, step))
+        assert _plan_sig(a) == _plan_sig(b)
+        a, b = _both(lambda: planner.solve_one_step_ahead(batch, prof, slo, step, paused=paused,
+                                                          deposit_snapshot=snap))
+        assert _plan_sig(a) == _plan_sig(b)
+
+
+def test_native_is_faster_at_b5():
+    rng = random.Random(5)
+    batch, prof, slo, paused, snap = _instance(rng, 32, 5)
+    t0 = time.perf_counter()
+    planner.SOLVER = "native"
+    a = planner.solve(batch, prof, slo, 1, paused=paused, deposit_snapshot=snap)
+    t_native = time.perf_counter() - t0
+    planner.SOLVER = "python"
+    t0 = time.perf_counter()
+    b = planner.solve(batch, prof, slo, 1, paused=paused, deposit_snapshot=snap)
+    t_py = time.perf_counter() - t0
+    planner.SOLVER = "native"
+    assert _plan_sig(a) == _plan_sig(b)
+    assert t_native < t_py
