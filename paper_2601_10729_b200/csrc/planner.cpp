@@ -382,57 +382,122 @@ struct Ranker {
 
   Ranker(const Problem& pr, int th) : P(pr), B(pr.p->batch), threads(th) {}
 
+  // Capacity-feasible candidates in lower-bound order (planner.py:310-341, :365-372).
+  // Depth-first over requests in enumeration order: resident blocks and every
+  // layer's offloaded demand only grow as requests are added, so a partial
+  // assignment already over budget prunes its whole subtree.  Subtrees of the
+  // first requests' choices run in parallel; concatenating them in root order
+  // keeps enumeration order.  The lower bound max(L*comp, fetch/bw) is then a
+  // stable counting sort on the integer fetch volume.
   bool build() {
     const Options& op = P.op;
     const int C = op.C, L = op.L;
-    int64_t total = 1;
-    for (int r = 0; r < B; ++r) total *= C;
     const int64_t budget = P.p->gpu_block_budget;
-    std::vector<std::vector<Cand>> part(std::max(1, threads));
-    std::atomic<int> slot{0};
-    parallel_for(total, threads, [&](int64_t lo, int64_t hi) {
-      std::vector<Cand>& out = part[slot.fetch_add(1)];
+    const int split = std::min(B, C >= 8 ? 2 : 3);
+    int64_t roots = 1;
+    for (int r = 0; r < split; ++r) roots *= C;
+    std::vector<std::vector<Cand>> part(roots);
+    std::atomic<int64_t> next_root{0};
+    auto worker = [&] {
+      std::vector<int64_t> demand((size_t)(B + 1) * L);
+      std::vector<int64_t> res(B + 1), fet(B + 1);
       int pick[64];
-      std::vector<int64_t> demand(L);
-      for (int64_t idx = lo; idx < hi; ++idx) {
-        decode(idx, C, B, pick);
-        int64_t resident = 0, fetch = 0;
-        for (int r = 0; r < B; ++r) {
-          resident += P.p->blocks[r] * (L - op.count[pick[r]]);
-          fetch += P.p->blocks[r] * op.count[pick[r]];
+      while (true) {
+        const int64_t root = next_root.fetch_add(1);
+        if (root >= roots) break;
+        std::vector<Cand>& out = part[root];
+        // decode the root prefix
+        int64_t rr = root;
+        for (int r = split - 1; r >= 0; --r) {
+          pick[r] = (int)(rr % C);
+          rr /= C;
         }
-        if (resident > budget) continue;
-        int64_t worst = 0;
-        std::fill(demand.begin(), demand.end(), 0);
-        for (int r = 0; r < B; ++r) {
-          if (op.count[pick[r]] == 0) continue;
-          const uint8_t* m = &op.mask[(size_t)pick[r] * L];
-          for (int l = 0; l < L; ++l)
-            if (m[l]) demand[l] += P.p->blocks[r];
+        std::fill(demand.begin(), demand.begin() + L, 0);
+        res[0] = fet[0] = 0;
+        bool ok = true;
+        for (int r = 0; r < split && ok; ++r) {
+          const int c = pick[r];
+          const int64_t sz = P.p->blocks[r];
+          res[r + 1] = res[r] + sz * (L - op.count[c]);
+          fet[r + 1] = fet[r] + sz * op.count[c];
+          int64_t worst = 0;
+          for (int l = 0; l < L; ++l) {
+            const int64_t v = demand[(size_t)r * L + l] + (op.mask[(size_t)c * L + l] ? sz : 0);
+            demand[(size_t)(r + 1) * L + l] = v;
+            worst = std::max(worst, v);
+          }
+          ok = res[r + 1] + worst <= budget;
         }
-        for (int l = 0; l < L; ++l) worst = std::max(worst, demand[l]);
-        if (resident + worst <= budget) out.push_back({idx, fetch});
+        if (!ok) continue;
+        if (split == B) {
+          out.push_back({root, fet[B]});
+          continue;
+        }
+        // iterative DFS below the root
+        int depth = split;
+        pick[depth] = -1;
+        while (depth >= split) {
+          const int c = ++pick[depth];
+          if (c >= C) {
+            --depth;
+            continue;
+          }
+          const int64_t sz = P.p->blocks[depth];
+          const int64_t rs = res[depth] + sz * (L - op.count[c]);
+          if (rs > budget) continue;
+          const int64_t* dprev = &demand[(size_t)depth * L];
+          int64_t* dnext = &demand[(size_t)(depth + 1) * L];
+          const uint8_t* m = &op.mask[(size_t)c * L];
+          int64_t worst = 0;
+          for (int l = 0; l < L; ++l) {
+            const int64_t v = dprev[l] + (m[l] ? sz : 0);
+            dnext[l] = v;
+            worst = std::max(worst, v);
+          }
+          if (rs + worst > budget) continue;
+          res[depth + 1] = rs;
+          fet[depth + 1] = fet[depth] + sz * op.count[c];
+          if (depth + 1 == B) {
+            int64_t idx = 0;
+            for (int r = 0; r < B; ++r) idx = idx * C + pick[r];
+            out.push_back({idx, fet[B]});
+          } else {
+            ++depth;
+            pick[depth] = -1;
+          }
+        }
       }
-    });
-    for (auto& v : part) cands.insert(cands.end(), v.begin(), v.end());
-    if (cands.empty()) return false;
-    // enumeration order, then stable by lower bound (np.argsort kind="stable")
-    std::sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) { return a.idx < b.idx; });
+    };
+    std::vector<std::thread> ts;
+    for (int t = 1; t < threads; ++t) ts.emplace_back(worker);
+    worker();
+    for (auto& th : ts) th.join();
+    size_t n = 0;
+    for (auto& v : part) n += v.size();
+    if (n == 0) return false;
+    // stable counting sort by lower bound: fetch/bw <= L*comp all tie at L*comp
     const double compL = P.comp * (double)L;
     const double bw = P.p->bandwidth_blocks_per_ms;
-    std::vector<double> bound(cands.size());
-    for (size_t i = 0; i < cands.size(); ++i)
-      bound[i] = std::max(compL, (double)cands[i].fetch / bw);
-    std::vector<size_t> ord(cands.size());
-    std::iota(ord.begin(), ord.end(), 0);
-    std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return bound[a] < bound[b]; });
-    std::vector<Cand> sorted(cands.size());
-    lb.resize(cands.size());
-    for (size_t i = 0; i < ord.size(); ++i) {
-      sorted[i] = cands[ord[i]];
-      lb[i] = bound[ord[i]];
+    int64_t max_f = 0;
+    for (auto& v : part)
+      for (auto& c : v) max_f = std::max(max_f, c.fetch);
+    auto key = [&](int64_t f) -> int64_t { return ((double)f / bw <= compL) ? 0 : f + 1; };
+    std::vector<int64_t> count((size_t)max_f + 2, 0);
+    for (auto& v : part)
+      for (auto& c : v) ++count[(size_t)key(c.fetch)];
+    int64_t run = 0;
+    for (auto& x : count) {
+      const int64_t k = x;
+      x = run;
+      run += k;
     }
-    cands.swap(sorted);
+    cands.resize(n);
+    for (auto& v : part) {
+      for (auto& c : v) cands[(size_t)count[(size_t)key(c.fetch)]++] = c;
+      std::vector<Cand>().swap(v);
+    }
+    lb.resize(n);
+    for (size_t i = 0; i < n; ++i) lb[i] = std::max(compL, (double)cands[i].fetch / bw);
     return true;
   }
 
