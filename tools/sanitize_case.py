@@ -1,0 +1,38 @@
+"""Small K1/K3/K2/K4 workload for compute-sanitizer (memcheck / racecheck / synccheck)."""
+import math
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "tests"))
+import torch  # noqa: E402
+
+from kvgen import make_case  # noqa: E402
+from paper_2601_10729_b200 import ops  # noqa: E402
+from paper_2601_10729_b200.core import PlacementMatrix, RequestState  # noqa: E402
+from paper_2601_10729_b200.executor import B200Executor, ModelShape  # noqa: E402
+
+dev = torch.device("cuda:0")
+for variant in ("stream", "split"):
+    ops.set_attention_kernel(variant)
+    for lens in ([700, 33, 1, 0, 255], [3000]):
+        case = make_case(lens, 8, 2, seed=1)
+        ops.decode_attention(case["q"].to(dev), case["pool"].to(dev),
+                             torch.from_numpy(case["block_tables"]).to(dev),
+                             torch.from_numpy(case["seq_lens"]).to(dev), scale=1 / math.sqrt(128))
+ops.set_attention_kernel("auto")
+shape = ModelShape(4, 8, 2)
+batch = [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=200 + 70 * i, target_output_tokens=8)
+         for i in range(3)]
+ex = B200Executor(shape, device_blocks=300, host_blocks=300)
+a = PlacementMatrix.from_strides([0, 1, 2], 4, [2, None, 1])
+b = PlacementMatrix.from_strides([0, 1, 2], 4, [None, 1, 2])
+ex.install(batch, a)
+ex.decode_step(batch, a)
+for r in batch:
+    r.record_generated_token()
+ex.install(batch, b)
+ex.decode_step(batch, b)
+torch.cuda.synchronize()
+ex.close()
+print("sanitize case done")
