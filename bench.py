@@ -45,6 +45,10 @@ CONFIGS = {
                  hidden=4096,
                  workload="Llama-3.1-8B shape (32 layers, 32q/8kv, d=128, bf16), B=16, 32K ctx, "
                           "stride-2 plan: 50% of layers' KV host-resident, 1xB200"),
+    "cfg2r": dict(layers=32, hq=32, hkv=8, batch=16, prompt=32760, strides=[None] * 16, output=64,
+                  hidden=4096,
+                  workload="Llama-3.1-8B shape, B=16, 32K ctx, every layer HBM-resident "
+                           "(pure K1 chain; HBM-bound reference point for cfg2)"),
     "cfg4": dict(layers=80, hq=64, hkv=8, batch=32, prompt=65528, strides="flexgen_plus",
                  output=64, hidden=8192,
                  workload="Llama-3.1-70B shape (80 layers, 64q/8kv, d=128, bf16), B=32, 64K ctx, "
@@ -463,6 +467,7 @@ def run_ours(args, cfg):
                           "frac_of_pcie5_nominal": host_alg / (ms_per_step * 1e-3) / 1e9
                           / PCIE5_NOMINAL_GBS,
                           "blocks_to_fetch_check": blocks_to_fetch(placement, batch)},
+        "attn_share_of_step": tm["acc_attn_ms"] / max(tm["acc_step_ms"], 1e-9),
         "gpu_launches": args.steps * (1 + L + len({l for row in placement.rows
                                                    for l, b in enumerate(row) if b == 0})),
         "clocks": clocks.summary(),

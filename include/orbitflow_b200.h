@@ -91,6 +91,16 @@ OFB_API int ofb_kv_append(const void* k_new, const void* v_new, void* kv_pool,
                   const uint64_t* host_slabs, int32_t num_layers, int32_t batch,
                   int32_t num_kv_heads, int32_t head_dim, void* stream);
 
+/* ---- K5: prefill KV written straight to its planned location ----------- */
+/* Scatter a request's prompt K/V (bf16 [L][tokens][Hkv][128] each, token-major
+ * as a prefill produces it) into the paged layout of L slabs whose base
+ * addresses are dst[L] (device array): an HBM extent for a resident layer, the
+ * mapped pinned host slab for an offloaded one - no staging, no second copy.
+ * Realises what the reference leaves free (kvsim/engine.py:495-503:
+ * prefill is only priced) and the paper's direct host write. */
+OFB_API int ofb_kv_prefill(const void* k, const void* v, const uint64_t* dst, int32_t num_layers,
+                           int32_t tokens, int32_t num_kv_heads, int32_t head_dim, void* stream);
+
 /* ---- K2 + K3 + K1: one decode step of the whole layer stack ------------ */
 typedef struct ofb_runtime ofb_runtime;
 

@@ -92,6 +92,7 @@ SIGNATURES = {
                                             c_i32, c_i32, c_i32, c_i32, c_i32, c_f32, c_vp]),
     "ofb_kv_append": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_i32,
                                      c_i32, c_vp]),
+    "ofb_kv_prefill": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp]),
     "ofb_runtime_create": (c_vp, [c_i32]),
     "ofb_runtime_destroy": (ctypes.c_int, [c_vp]),
     "ofb_runtime_decode_step": (ctypes.c_int, [c_vp, ctypes.POINTER(StepDesc), c_vp]),

@@ -72,6 +72,8 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
   const int warp = tid >> 5;
   const int lane = tid & 31;
 
+  pdl_wait();     // see decode_attention_stream.cu: predecessor must be complete
+  pdl_trigger();
   const int seq = a.seq_lens[req];
   const int nblk = (seq + kBlockTokens - 1) / kBlockTokens;
   const int nsplit = (nblk + a.blocks_per_split - 1) / a.blocks_per_split;
@@ -428,6 +430,15 @@ static bool use_split_kernel(int batch, int hkv, int max_seq_len) {
   return v == 1;
 }
 
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* v = std::getenv("OFB_PDL");
+    on = (v && std::strcmp(v, "0") == 0) ? 0 : 1;
+  }
+  return on == 1;
+}
+
 int set_attention_variant(int variant) {
   const int prev = k1_variant();
   if (variant >= 0 && variant <= 2) g_k1_variant = variant;
@@ -493,8 +504,17 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
   a.max_splits = ws_splits;
   a.scale_log2 = scale * 1.4426950408889634f;
   dim3 grid(plan.max_splits, hkv, batch);
-  paged_gqa_decode_kernel<<<grid, kAttnThreads, kAttnSmemBytes, stream>>>(map, a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kAttnThreads);
+  cfg.dynamicSmemBytes = kAttnSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, paged_gqa_decode_kernel, map, a);
 }
 
 int attention_occupancy() {

@@ -117,6 +117,11 @@ paged_gqa_decode_stream_kernel(const __grid_constant__ CUtensorMap kv_map, const
     fence_mbar_init();
   }
   __syncthreads();
+  // Everything above touched only launch inputs; the previous kernel on the
+  // stream (an append into this layer's slabs, an o-projection producing q,
+  // the previous layer's K1 sharing this workspace) must be complete past here.
+  pdl_wait();
+  pdl_trigger();
 
   // Effective grid: the host sized it for max_seq_len; with shorter actual
   // sequences keep >= 1 tile per CTA so no CTA range is empty (ticket counts
@@ -361,8 +366,17 @@ cudaError_t launch_decode_attention_stream(const CUtensorMap& map, const void* q
   a.group = hq / hkv;
   a.grid = stream_grid(batch, hkv, max_seq_len);
   a.scale_log2 = scale * 1.4426950408889634f;
-  paged_gqa_decode_stream_kernel<<<a.grid, kSThreads, kSSmemBytes, stream>>>(map, a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.grid);
+  cfg.blockDim = dim3(kSThreads);
+  cfg.dynamicSmemBytes = kSSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, paged_gqa_decode_stream_kernel, map, a);
 }
 
 }  // namespace ofb

@@ -32,6 +32,8 @@ cudaError_t launch_kv_append(const void* k_new, const void* v_new, void* pool,
                              cudaStream_t stream);
 int attention_occupancy();
 int set_attention_variant(int variant);
+cudaError_t launch_kv_prefill(const void* k, const void* v, const uint64_t* dst, int num_layers,
+                              int tokens, int hkv, cudaStream_t stream);
 }  // namespace ofb
 
 namespace {
@@ -354,6 +356,17 @@ int ofb_kv_append(const void* k_new, const void* v_new, void* kv_pool,
                                         positions, host_slabs, num_layers, batch, num_kv_heads,
                                         /*kAppendAll*/ 1, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "kv_append_kernel launch");
+  return 0;
+}
+
+int ofb_kv_prefill(const void* k, const void* v, const uint64_t* dst, int32_t num_layers,
+                   int32_t tokens, int32_t num_kv_heads, int32_t head_dim, void* stream) {
+  if (head_dim != ofb::kHeadDim) return fail(-1, "head_dim must be 128");
+  if (!k || !v || !dst) return fail(-1, "ofb_kv_prefill: null pointer");
+  if (num_layers < 0 || tokens < 0 || num_kv_heads <= 0) return fail(-1, "ofb_kv_prefill: bad sizes");
+  cudaError_t e = ofb::launch_kv_prefill(k, v, dst, num_layers, tokens, num_kv_heads,
+                                         static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "kv_prefill_kernel launch");
   return 0;
 }
 

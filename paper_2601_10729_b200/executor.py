@@ -128,28 +128,34 @@ class B200Executor:
         return cls(shape, device_blocks=device_blocks, host_blocks=host_blocks,
                    staging_slots=staging_slots, **kw)
 
-    # ------------------------------------------------------------ synthetic KV
-    def _fill_tensor(self, rid: int, layer: int, blocks: int) -> torch.Tensor:
-        g = torch.Generator(device=self.device)
-        g.manual_seed((self.seed * 1_000_003 + rid) * 4099 + layer)
-        shape = (blocks, self.shape.num_kv_heads, 2, BLOCK_TOKENS, HEAD_DIM)
-        if self.fill == "zeros":
-            return torch.zeros(shape, dtype=torch.bfloat16, device=self.device)
-        return torch.randn(shape, generator=g, device=self.device, dtype=torch.float32).to(torch.bfloat16)
+    # ------------------------------------------------------------ prefill (K5)
+    def _prefill(self, rid: int, tokens: int, dsts: list[int]) -> None:
+        """Write a fresh request's prompt KV straight to its planned slabs (K5).
 
-    def _prefill_device(self, rid: int, layer: int, start: int, used: int) -> None:
-        if used:
-            self.pool.tensor[start:start + used].copy_(self._fill_tensor(rid, layer, used))
-
-    def _prefill_host(self, rid: int, layer: int, hstart: int, used: int) -> None:
-        if not used:
+        The prompt K/V a prefill would produce (token-major, per layer) is
+        synthetic here (seeded N(0,1)); ``dsts[l]`` is the HBM extent or the
+        mapped host slab of layer l, so offloaded layers never touch HBM.
+        """
+        if tokens <= 0:
             return
-        src = self._fill_tensor(rid, layer, used)
-        self.runtime.migrate(np.array([self.host.addr(hstart)], dtype=np.uint64),
-                             np.array([src.data_ptr()], dtype=np.uint64),
-                             np.array([used * self.shape.block_bytes], dtype=np.int64),
-                             np.array([1], dtype=np.int32))
-        self.runtime.migration_pending(wait=True)  # src is a temporary
+        from . import ops
+
+        hkv = self.shape.num_kv_heads
+        per_layer = tokens * hkv * HEAD_DIM * 2 * 2      # K + V bytes of one layer
+        chunk = max(1, (1 << 30) // per_layer)
+        for lo in range(0, len(dsts), chunk):
+            hi = min(len(dsts), lo + chunk)
+            shape = (hi - lo, tokens, hkv, HEAD_DIM)
+            if self.fill == "zeros":
+                k = torch.zeros(shape, dtype=torch.bfloat16, device=self.device)
+                v = torch.zeros(shape, dtype=torch.bfloat16, device=self.device)
+            else:
+                g = torch.Generator(device=self.device)
+                g.manual_seed((self.seed * 1_000_003 + rid) * 4099 + lo)
+                k = torch.randn(shape, generator=g, device=self.device).to(torch.bfloat16)
+                v = torch.randn(shape, generator=g, device=self.device).to(torch.bfloat16)
+            dst = torch.tensor(dsts[lo:hi], dtype=torch.int64).to(self.device)
+            ops.kv_prefill(k, v, dst)
 
     # ------------------------------------------------------------ HBM extents
     def _reclaim(self, wait: bool) -> None:
@@ -193,27 +199,33 @@ class B200Executor:
                 continue
             fresh = rid not in self.slabs
             st = self._ensure(req)
+            if fresh:
+                # prefill KV goes straight to its placed location
+                dsts = []
+                for layer, loc in enumerate(locs):
+                    if loc in _DEVICE_LOCS:
+                        st.dev[layer] = self._alloc_dev(st.capacity)
+                        dsts.append(self.pool.addr(st.dev[layer]))
+                    else:
+                        st.host[layer] = self.host.alloc.alloc(st.capacity)
+                        dsts.append(self.host.addr(st.host[layer]))
+                self._prefill(rid, req.total_tokens, dsts)
+                continue
             used = blocks_for_tokens(req.total_tokens, BLOCK_TOKENS)
             nbytes = used * self.shape.block_bytes
             for layer, loc in enumerate(locs):
                 on_dev = st.dev[layer] is not None
-                if loc in _DEVICE_LOCS and not on_dev:
+                if loc in _DEVICE_LOCS and not on_dev:       # restore (H2D)
                     start = self._alloc_dev(st.capacity)
                     st.dev[layer] = start
-                    if fresh or st.host[layer] is None:
-                        self._prefill_device(rid, layer, start, used)
-                    else:
-                        moves.append((self.pool.addr(start), self.host.addr(st.host[layer]), nbytes, 0))
-                elif loc not in _DEVICE_LOCS:
+                    moves.append((self.pool.addr(start), self.host.addr(st.host[layer]), nbytes, 0))
+                elif loc not in _DEVICE_LOCS and on_dev:     # evict (D2H)
                     if st.host[layer] is None:
                         st.host[layer] = self.host.alloc.alloc(st.capacity)
-                        if not on_dev:
-                            self._prefill_host(rid, layer, st.host[layer], used)
-                    if on_dev:
-                        moves.append((self.host.addr(st.host[layer]), self.pool.addr(st.dev[layer]),
-                                      nbytes, 1))
-                        evicted.append((st.dev[layer], st.capacity))
-                        st.dev[layer] = None
+                    moves.append((self.host.addr(st.host[layer]), self.pool.addr(st.dev[layer]),
+                                  nbytes, 1))
+                    evicted.append((st.dev[layer], st.capacity))
+                    st.dev[layer] = None
         if moves:
             if self._mig_start is None:
                 self._mig_start = torch.cuda.Event(enable_timing=True)

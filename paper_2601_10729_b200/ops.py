@@ -131,3 +131,14 @@ def set_attention_kernel(variant: str) -> str:
     if prev < 0:
         _native.check(prev, "ofb_set_attention_kernel")
     return {v: k for k, v in names.items()}[prev]
+
+
+def kv_prefill(k: torch.Tensor, v: torch.Tensor, dst_addrs: torch.Tensor) -> None:
+    """K5: scatter prompt K/V (bf16 [L, P, Hkv, 128]) into the paged layout of the
+    L slabs at ``dst_addrs`` (int64 device tensor of HBM or mapped-host addresses)."""
+    _need_cuda(k, v, dst_addrs)
+    layers, tokens, hkv, d = k.shape
+    lib = _native.load()
+    rc = lib.ofb_kv_prefill(k.contiguous().data_ptr(), v.contiguous().data_ptr(),
+                            dst_addrs.data_ptr(), layers, tokens, hkv, d, _stream_ptr())
+    _native.check(rc, "ofb_kv_prefill")

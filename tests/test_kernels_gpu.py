@@ -160,3 +160,34 @@ def test_max_seq_len_overestimate_and_tiny_work():
     case = make_case([5, 3], 8, 2, seed=6, max_blocks=4096)   # W = 2 tiles, grid sized for 64K
     got = _run_gpu(case, max_seq_len=65536)
     np.testing.assert_allclose(got, _run_oracle(case), rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("tokens", [1, 16, 37, 300])
+def test_prefill_writes_paged_layout_to_device_and_host(tokens):
+    """K5 scatters token-major prompt K/V into the paged block layout, to an HBM
+    extent and to a mapped pinned host slab alike (bit-exact)."""
+    from paper_2601_10729_b200 import ops
+    from paper_2601_10729_b200.kvpool import HostArena
+
+    L, hkv = 3, 2
+    nblk = (tokens + 15) // 16
+    g = torch.Generator().manual_seed(tokens)
+    k = torch.randn((L, tokens, hkv, D), generator=g).to(torch.bfloat16)
+    v = torch.randn((L, tokens, hkv, D), generator=g).to(torch.bfloat16)
+    dev = torch.device("cuda:0")
+    pool = torch.zeros((2 * nblk, hkv, 2, 16, D), dtype=torch.bfloat16, device=dev)
+    block_bytes = hkv * 8192
+    arena = HostArena(nblk, block_bytes)
+    try:
+        dsts = [pool.data_ptr(), pool.data_ptr() + nblk * block_bytes, arena.base]
+        ops.kv_prefill(k.to(dev), v.to(dev), torch.tensor(dsts, dtype=torch.int64).to(dev))
+        torch.cuda.synchronize()
+        slabs = [bf16_bits(pool[:nblk].cpu()), bf16_bits(pool[nblk:].cpu()),
+                 arena.view_u16(0, nblk).reshape(nblk, hkv, 2, 16, D).copy()]
+        for l in range(L):
+            for t in range(tokens):
+                for h in range(hkv):
+                    np.testing.assert_array_equal(slabs[l][t // 16, h, 0, t % 16], bf16_bits(k[l, t, h]))
+                    np.testing.assert_array_equal(slabs[l][t // 16, h, 1, t % 16], bf16_bits(v[l, t, h]))
+    finally:
+        arena.close()
