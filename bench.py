@@ -146,7 +146,12 @@ def _measured_peaks():
 def _ncu_traffic(alg_bytes):
     """DRAM bytes per K1 launch from the committed ncu --set full capture of the
     same layer shape (profiles/), scaled to this launch's algorithmic bytes."""
-    for path in sorted((ROOT / "profiles").glob("*k1_ncu_full_cfg2layer.json"), reverse=True):
+    from paper_2601_10729_b200 import ops
+
+    paths = sorted((ROOT / "profiles").glob("*ncu_full_cfg2layer.json"), reverse=True)
+    # the capture of the K1 variant that auto-selection runs at this shape first
+    paths.sort(key=lambda p: ("stream" not in p.name))
+    for path in paths:
         try:
             rec = json.loads(path.read_text())[0]
             unit = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
@@ -274,12 +279,15 @@ def run_ours(args, cfg):
     from paper_2601_10729_b200.runtime import link_probe
 
     rank, world, local = _env_rank()
+    # one rank per GPU; OFB_DIST_BACKEND=gloo + several ranks per GPU is only for
+    # exercising the multi-rank path on a single-GPU box (tests), never for numbers
+    local = local % max(1, torch.cuda.device_count())
     dist = None
     if world > 1:
         import torch.distributed as dist  # noqa: F811
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("OFB_DIST_BACKEND", "nccl"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 

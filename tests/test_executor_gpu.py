@@ -226,3 +226,27 @@ def test_live_mode_engine_runs_on_measured_time():
     rep = collect_metrics(log)
     assert rep.requests_finished == 4 and rep.tokens_delivered == 20
     ex.close()
+
+
+def test_bench_multi_rank_path_on_one_gpu():
+    """torchrun N=2 through bench.py's TP path (KV-head shards, per-layer o-proj +
+    all-reduce, max-over-ranks timing, rank-0 JSON) with gloo so both ranks can
+    share the single GPU of this box - exercises the N>1 code the 8-GPU run uses."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, OFB_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29513", str(root / "bench.py"),
+           "--gpus", "2", "--config", "cfg1", "--steps", "3", "--warmup", "3"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert "tp2" in line["config"]["parallelism"] and line["value"] > 0
