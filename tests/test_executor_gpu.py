@@ -250,3 +250,28 @@ def test_bench_multi_rank_path_on_one_gpu():
     line = json.loads(lines[0])
     assert line["n_gpus"] == 2 and line["scaling"] == "strong"
     assert "tp2" in line["config"]["parallelism"] and line["value"] > 0
+
+
+def test_cli_simulate_on_b200_and_report_rerender(tmp_path):
+    """`kvsim simulate --executor b200` runs every decode step on the GPU; its NDJSON
+    event log (with measured_us per step) re-renders byte-stably via `report`."""
+    from paper_2601_10729_b200.cli import main
+    from paper_2601_10729_b200.metrics import load_log
+
+    trace = tmp_path / "t.trace"
+    assert main(["gen-trace", "--out", str(trace), "--rate", "400", "--seed", "3", "--count", "6",
+                 "--prompt-median", "120", "--output-median", "8", "--max-prompt", "400",
+                 "--max-output", "16"]) == 0
+    report, log_path = tmp_path / "r.json", tmp_path / "run.log"
+    assert main(["simulate", "--trace", str(trace), "--policy", "orbit", "--executor", "b200",
+                 "--report", str(report), "--event-log", str(log_path)]) == 0
+    steps = [r for r in load_log(log_path) if r["kind"] == "step"]
+    assert steps and all("measured_us" in r["payload"] for r in steps)
+    again = tmp_path / "again.json"
+    assert main(["report", "--event-log", str(log_path), "--out", str(again)]) == 0
+    assert again.read_bytes() == report.read_bytes()
+    # decisions equal the model-only run of the same trace
+    model_report = tmp_path / "m.json"
+    assert main(["simulate", "--trace", str(trace), "--policy", "orbit", "--report",
+                 str(model_report)]) == 0
+    assert model_report.read_bytes() == report.read_bytes()
