@@ -275,3 +275,72 @@ def test_cli_simulate_on_b200_and_report_rerender(tmp_path):
     assert main(["simulate", "--trace", str(trace), "--policy", "orbit", "--report",
                  str(model_report)]) == 0
     assert model_report.read_bytes() == report.read_bytes()
+
+
+@pytest.mark.parametrize("policy", ["orbit", "dynamic_heuristic", "flexgen_plus", "deepspeed_like"])
+def test_policies_with_deferral_and_preemption_under_executor(policy):
+    """Tight budget: Orbit pauses/resumes (lazy eviction of removable layers, K4),
+    baselines preempt (KV dropped, request re-prefilled on re-admission).  Decisions
+    stay identical to the model-only run and residency equals the table each step."""
+    from paper_2601_10729_b200.executor import B200Executor, ModelShape
+
+    prof = SystemProfile(num_layers=6, compute_base_ms=0.3, compute_per_token_ms=0.002,
+                         bandwidth_blocks_per_ms=4.0, gpu_block_budget=140, block_size=16,
+                         prefill_per_token_ms=0.002)
+    slo = SloConfig(tbt_target_ms=4.0, tpot_target_ms=4.0, window_min=2, window_max=6)
+    trace = workload.Trace(tuple(workload.TraceRequest(i * 2, 150 + 45 * i, 4 + i % 4)
+                                 for i in range(8)), {})
+    cfg = RunConfig(max_batch=4)
+
+    def run(executor):
+        pol = make_policy(PolicyKind(policy), prof, slo, max_batch=4, token_cap=cfg.batch_token_cap)
+        return Simulation(trace, pol, prof, slo, cfg, executor=executor).execute()
+
+    ref = run(None)
+
+    class Checked(B200Executor):
+        def decode_step(self, batch, placement=None, inputs=None, sync=True):
+            ms = super().decode_step(batch, placement, inputs, sync)
+            for req, row in zip(batch, placement.rows):
+                assert self.residency(req.id) == ["dev" if b else "host" for b in row]
+            return ms
+
+    ex = Checked.for_trace(trace, prof, shape=ModelShape(6, 8, 2), max_batch=4)
+    log = run(ex)
+    strip = [dict(r, payload={k: v for k, v in r["payload"].items() if k != "measured_us"})
+             if r["kind"] == "step" else r for r in log]
+    assert strip == ref
+    kinds = {r["kind"] for r in ref}
+    if policy == "orbit":
+        assert "pause" in kinds or "replan" in kinds
+    ex.close()
+
+
+def test_reactive_preemption_releases_and_reprefills():
+    """flexgen_like with a static stride that stops fitting: the engine preempts the
+    youngest request (KV dropped, executor.release), re-admits and re-prefills it;
+    decisions identical to the model-only run."""
+    from paper_2601_10729_b200.executor import B200Executor, ModelShape
+    from paper_2601_10729_b200.policies import PolicyOptions
+
+    prof = SystemProfile(num_layers=6, compute_base_ms=0.3, compute_per_token_ms=0.002,
+                         bandwidth_blocks_per_ms=4.0, gpu_block_budget=80, block_size=16,
+                         prefill_per_token_ms=0.002)
+    slo = SloConfig(tbt_target_ms=4.0, tpot_target_ms=4.0, window_min=2, window_max=6)
+    trace = workload.Trace(tuple(workload.TraceRequest(i * 2, 150 + 45 * i, 4 + i % 4)
+                                 for i in range(8)), {})
+    opts = PolicyOptions(static_stride=None, worst_case_tokens=600)
+
+    def run(executor):
+        pol = make_policy(PolicyKind.FLEXGEN_LIKE, prof, slo, opts, max_batch=4)
+        return Simulation(trace, pol, prof, slo, RunConfig(max_batch=4), executor=executor).execute()
+
+    ref = run(None)
+    assert sum(1 for r in ref if r["kind"] == "preempt") >= 1
+    ex = B200Executor.for_trace(trace, prof, shape=ModelShape(6, 8, 2), max_batch=4)
+    log = run(ex)
+    strip = [dict(r, payload={k: v for k, v in r["payload"].items() if k != "measured_us"})
+             if r["kind"] == "step" else r for r in log]
+    assert strip == ref
+    assert not ex.slabs            # everything released at the end
+    ex.close()
