@@ -196,6 +196,49 @@ OFB_API int ofb_runtime_migration_pending(ofb_runtime* rt, int32_t wait);
 OFB_API int ofb_runtime_timing(ofb_runtime* rt, ofb_step_timing* out);
 OFB_API int ofb_runtime_timing_reset(ofb_runtime* rt);
 
+/* ---- K6 / C1: o-projection + all-reduce over peer memory (TP) ----------- */
+/* after each layer's attention a KV-head-sharded rank holds
+ * attn[B, Hq/N * 128] for its own heads; the decoder needs
+ * hidden[B, H] = sum over ranks of attn_r @ W_o[rows of r]^T.  The reference
+ * has no multi-GPU path; the paper runs NCCL after the projection
+ * (PAPER.md:727-729).  One kernel does both: tcgen05 tensor cores compute this
+ * rank's partial tile by tile (TMA-staged W_o rows, accumulator in TMEM) and
+ * each finished tile is pushed straight into every peer's inbox over
+ * NVLink (P2P stores into IPC-mapped symmetric buffers) and flagged; the last
+ * CTA of a tile sums the world's copies of it in rank order, so every rank
+ * ends with a bit-identical hidden state and the exchange overlaps the math
+ * tile by tile.  world = 1 is the projection alone. */
+
+/* Symmetric (IPC-shareable) device buffer: cudaMalloc'd, zeroed. */
+OFB_API int ofb_symm_alloc(int64_t bytes, void** ptr);
+OFB_API int ofb_symm_free(void* ptr);
+/* CUDA IPC: 64-byte handle of a symm buffer; open a peer's handle (P2P enabled). */
+OFB_API int ofb_ipc_get_handle(void* ptr, void* handle64);
+OFB_API int ofb_ipc_open_handle(const void* handle64, void** ptr);
+OFB_API int ofb_ipc_close_handle(void* ptr);
+
+/* Bytes of each rank's symmetric buffer (inbox [2][world][hidden/128][max_batch][128]
+ * bf16 + flags) and of its private workspace (split-K partials + tile tickets;
+ * zero it once). */
+OFB_API int64_t ofb_oproj_symm_bytes(int32_t world, int32_t max_batch, int32_t hidden);
+OFB_API int64_t ofb_oproj_workspace_bytes(int32_t max_batch, int32_t k, int32_t hidden);
+
+typedef struct ofb_oproj_desc {
+  const void* x;       /* bf16 [layers][batch][k]: this rank's attention output, heads flattened */
+  const void* w;       /* bf16 [layers][hidden][k]: W_o rows of this rank's heads (Linear layout) */
+  void* out;           /* bf16 [batch][hidden]: the all-reduced result (same bits on every rank) */
+  int32_t layers, layer, batch, k, hidden;
+  void* workspace;
+  int64_t workspace_bytes;
+  int32_t world, rank, max_batch;   /* world <= 8; batch <= max_batch <= 256 */
+  void* symm[8];       /* symm[r] = rank r's symmetric buffer as mapped here; symm[rank] local */
+  uint32_t epoch;      /* > 0, +1 per call, identical on every rank */
+  int32_t* status;     /* device int32: set to 1 if a peer's tile never arrived (timeout) */
+  int64_t timeout_ns;  /* spin limit per tile wait (0 = 5 s) */
+} ofb_oproj_desc;
+
+OFB_API int ofb_oproj_allreduce(const ofb_oproj_desc* desc, void* stream);
+
 /* ---- native exact placement solver (host code, no GPU needed) ---------- */
 /* Bit-exact restatement of kvsim solve / solve_capacity_only
  * (kvsim/planner.py:437-560), multithreaded.  Balances follow the reference's

@@ -79,6 +79,18 @@ class PlanResult(ctypes.Structure):
                 ("candidates_ranked", c_i64)]
 
 
+class OprojDesc(ctypes.Structure):
+    """Mirror of ``ofb_oproj_desc``."""
+
+    _fields_ = [
+        ("x", c_vp), ("w", c_vp), ("out", c_vp),
+        ("layers", c_i32), ("layer", c_i32), ("batch", c_i32), ("k", c_i32), ("hidden", c_i32),
+        ("workspace", c_vp), ("workspace_bytes", c_i64),
+        ("world", c_i32), ("rank", c_i32), ("max_batch", c_i32),
+        ("symm", c_vp * 8), ("epoch", ctypes.c_uint32), ("status", c_vp), ("timeout_ns", c_i64),
+    ]
+
+
 # name -> (restype, argtypes); exactly the symbols include/orbitflow_b200.h declares
 SIGNATURES = {
     "ofb_version": (ctypes.c_char_p, []),
@@ -103,6 +115,14 @@ SIGNATURES = {
     "ofb_runtime_timing": (ctypes.c_int, [c_vp, ctypes.POINTER(StepTiming)]),
     "ofb_runtime_migration_pending": (ctypes.c_int, [c_vp, c_i32]),
     "ofb_runtime_timing_reset": (ctypes.c_int, [c_vp]),
+    "ofb_symm_alloc": (ctypes.c_int, [c_i64, ctypes.POINTER(c_vp)]),
+    "ofb_symm_free": (ctypes.c_int, [c_vp]),
+    "ofb_ipc_get_handle": (ctypes.c_int, [c_vp, c_vp]),
+    "ofb_ipc_open_handle": (ctypes.c_int, [c_vp, ctypes.POINTER(c_vp)]),
+    "ofb_ipc_close_handle": (ctypes.c_int, [c_vp]),
+    "ofb_oproj_symm_bytes": (c_i64, [c_i32, c_i32, c_i32]),
+    "ofb_oproj_workspace_bytes": (c_i64, [c_i32, c_i32, c_i32]),
+    "ofb_oproj_allreduce": (ctypes.c_int, [ctypes.POINTER(OprojDesc), c_vp]),
     "ofb_plan_solve": (ctypes.c_int, [ctypes.POINTER(PlanProblem), ctypes.POINTER(PlanResult)]),
     "ofb_plan_last_error": (ctypes.c_char_p, []),
     "ofb_link_probe": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, ctypes.POINTER(c_f64),

@@ -1,0 +1,189 @@
+"""C1 on B200: the tensor-parallel o-projection fused with its all-reduce (K6).
+
+SURVEY.md 8(e): a KV-head-sharded rank ends each layer's attention with
+``attn[B, Hq/N, 128]`` for its own heads; the decoder needs
+``hidden[B, H] = sum_r attn_r @ W_o[rows of r]``.  The paper runs NCCL after
+the projection.  Here one sm_100a kernel
+(``csrc/oproj_allreduce.cu``) computes this rank's partial on the tcgen05
+tensor cores and pushes every finished tile straight into each peer's inbox
+over NVLink (CUDA-IPC-mapped symmetric buffers), so the exchange overlaps the
+math tile by tile; every rank sums the world's tiles in rank order and holds
+bit-identical results.
+
+``SymmetricBuffers`` owns this rank's buffer and maps the peers' (handles are
+exchanged once with ``torch.distributed.all_gather_object``, any backend).
+``SymmetricBuffers.emulated`` gives N ranks inside one process on one GPU -
+the only multi-rank configuration a single-GPU box can run - with the kernel
+and protocol unchanged (peer pointers are simply local).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _native
+
+MAX_WORLD = 8
+
+
+def _lib():
+    return _native.load()
+
+
+def _check(rc: int, what: str) -> None:
+    _native.check(rc, what)
+
+
+class SymmetricBuffers:
+    """One rank's IPC-shareable inbox/flags buffer plus every peer's, mapped here."""
+
+    def __init__(self, world: int, rank: int, max_batch: int, hidden: int, *, group=None,
+                 device=None, _peers=None, _owned=True):
+        if not 1 <= world <= MAX_WORLD:
+            raise ValueError(f"world must be 1..{MAX_WORLD}")
+        if not 0 <= rank < world:
+            raise ValueError("rank out of range")
+        if hidden % 128 or not 1 <= max_batch <= 256:
+            raise ValueError("hidden must be a multiple of 128 and 1 <= max_batch <= 256")
+        self.world, self.rank = world, rank
+        self.max_batch, self.hidden = max_batch, hidden
+        self.device = torch.device(device if device is not None else torch.cuda.current_device())
+        self.epoch = 0
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._opened: list[int] = []
+        self._owned = _owned
+        lib = _lib()
+        self._emulated = _peers is not None
+        if _peers is not None:           # emulated group: pointers supplied by the factory
+            self.ptrs = list(_peers)
+            self.local = self.ptrs[rank]
+            return
+        nbytes = int(lib.ofb_oproj_symm_bytes(world, max_batch, hidden))
+        if nbytes <= 0:
+            raise ValueError("bad symmetric-buffer geometry")
+        with torch.cuda.device(self.device):
+            p = ctypes.c_void_p()
+            _check(lib.ofb_symm_alloc(nbytes, ctypes.byref(p)), "ofb_symm_alloc")
+            self.local = p.value
+            self.ptrs = [None] * world
+            self.ptrs[rank] = self.local
+            if world > 1:
+                import torch.distributed as dist
+
+                handle = (ctypes.c_char * 64)()
+                _check(lib.ofb_ipc_get_handle(self.local, handle), "ofb_ipc_get_handle")
+                gathered = [None] * world
+                dist.all_gather_object(gathered, bytes(handle), group=group)
+                for r, h in enumerate(gathered):
+                    if r == rank:
+                        continue
+                    buf = (ctypes.c_char * 64).from_buffer_copy(h)
+                    q = ctypes.c_void_p()
+                    _check(lib.ofb_ipc_open_handle(buf, ctypes.byref(q)), f"ofb_ipc_open_handle(rank {r})")
+                    self.ptrs[r] = q.value
+                    self._opened.append(q.value)
+
+    @classmethod
+    def emulated(cls, world: int, max_batch: int, hidden: int, device=None) -> list["SymmetricBuffers"]:
+        """N ranks in this process on one GPU (tests / single-GPU boxes)."""
+        lib = _lib()
+        nbytes = int(lib.ofb_oproj_symm_bytes(world, max_batch, hidden))
+        dev = torch.device(device if device is not None else torch.cuda.current_device())
+        ptrs = []
+        with torch.cuda.device(dev):
+            for _ in range(world):
+                p = ctypes.c_void_p()
+                _check(lib.ofb_symm_alloc(nbytes, ctypes.byref(p)), "ofb_symm_alloc")
+                ptrs.append(p.value)
+        return [cls(world, r, max_batch, hidden, device=dev, _peers=ptrs, _owned=(r == 0))
+                for r in range(world)]
+
+    def next_epoch(self) -> int:
+        self.epoch = (self.epoch % 0xFFFFFFFF) + 1
+        return self.epoch
+
+    def check(self) -> None:
+        """Raise if any exchange timed out waiting for a peer (synchronises)."""
+        if int(self.status.item()) != 0:
+            raise RuntimeError(f"rank {self.rank}: a peer's tile never arrived (C1 exchange timed out)")
+
+    def close(self) -> None:
+        lib = _lib()
+        torch.cuda.synchronize(self.device)
+        for p in self._opened:
+            lib.ofb_ipc_close_handle(p)
+        self._opened.clear()
+        for p in self._freed_on_close():
+            lib.ofb_symm_free(p)
+        self.ptrs = []
+        self._owned = False
+
+    def _freed_on_close(self) -> list:
+        if not self._owned:
+            return []
+        if self._emulated:          # rank 0 of an emulated group owns every buffer
+            return [p for p in self.ptrs if p]
+        return [self.local]
+
+
+class OprojAllReduce:
+    """K6: ``hidden[B, H] = sum over ranks of x_r[B, K] @ W_r[H, K]^T`` per layer.
+
+    ``w_o``: bf16 [L, H, K] - the o-projection rows of this rank's heads in
+    ``nn.Linear`` layout (K = local q heads x 128).  ``symm=None`` is a single
+    rank (the projection alone, no exchange).
+    """
+
+    def __init__(self, w_o: torch.Tensor, max_batch: int, symm: SymmetricBuffers | None = None):
+        if not w_o.is_cuda or w_o.dtype != torch.bfloat16 or w_o.dim() != 3:
+            raise ValueError("w_o must be a bf16 CUDA tensor [layers, hidden, k]")
+        self.w = w_o.contiguous()
+        self.layers, self.hidden, self.k = self.w.shape
+        if self.k % 64 or self.hidden % 128:
+            raise ValueError("k must be a multiple of 64 and hidden of 128")
+        if symm is not None and (symm.hidden != self.hidden or symm.max_batch < max_batch):
+            raise ValueError("symmetric buffers sized for another hidden / batch")
+        self.max_batch = max_batch
+        self.symm = symm
+        lib = _lib()
+        nbytes = int(lib.ofb_oproj_workspace_bytes(max_batch, self.k, self.hidden))
+        self.ws = torch.zeros(nbytes, dtype=torch.uint8, device=self.w.device)
+        self._status = symm.status if symm is not None else torch.zeros(1, dtype=torch.int32,
+                                                                         device=self.w.device)
+
+    def __call__(self, x: torch.Tensor, layer: int, out: torch.Tensor | None = None,
+                 stream=None) -> torch.Tensor:
+        """``x``: bf16 [L, B, K] (or [L, B, Hq_local, 128]) - all layers' attention
+        output; layer ``layer`` is projected.  Returns bf16 [B, H]."""
+        if not x.is_cuda or x.dtype != torch.bfloat16:
+            raise ValueError("x must be a bf16 CUDA tensor (no CPU fallback)")
+        if x.shape[0] != self.layers:
+            raise ValueError("x must hold every layer: [layers, batch, ...]")
+        b = x.shape[1]
+        x = x.reshape(self.layers, b, -1)
+        if x.shape[2] != self.k or not x.is_contiguous():
+            raise ValueError(f"x must be contiguous [layers, batch, {self.k}]")
+        if out is None:
+            out = torch.empty((b, self.hidden), dtype=torch.bfloat16, device=x.device)
+        d = _native.OprojDesc()
+        d.x, d.w, d.out = x.data_ptr(), self.w.data_ptr(), out.data_ptr()
+        d.layers, d.layer, d.batch, d.k, d.hidden = self.layers, layer, b, self.k, self.hidden
+        d.workspace, d.workspace_bytes = self.ws.data_ptr(), self.ws.numel()
+        d.max_batch = self.max_batch
+        d.status = self._status.data_ptr()
+        d.timeout_ns = 0
+        if self.symm is None or self.symm.world == 1:
+            d.world, d.rank, d.epoch = 1, 0, 1
+            if self.symm is not None:
+                d.symm[0] = self.symm.local
+        else:
+            d.world, d.rank = self.symm.world, self.symm.rank
+            for r, p in enumerate(self.symm.ptrs):
+                d.symm[r] = p
+            d.epoch = self.symm.next_epoch()
+        s = stream if stream is not None else torch.cuda.current_stream(x.device)
+        _check(_lib().ofb_oproj_allreduce(ctypes.byref(d), ctypes.c_void_p(s.cuda_stream)),
+               "ofb_oproj_allreduce")
+        return out

@@ -1,0 +1,525 @@
+// K6 / C1: tensor-parallel o-projection fused with its all-reduce over peer
+// memory (PAPER.md:727-729 runs NCCL after the projection).
+//
+// hidden[B, H] = sum_r attn_r[B, K] @ W_r[H, K]^T, K = (Hq/N)*128 per rank.
+// At decode B is 16-64, so the GEMM is a weight stream (16 MiB of W_o per
+// layer at 70B/TP8) - HBM bound at 2*B flop per W byte.  It runs "swap AB" on
+// the 5th-gen tensor cores: UMMA M = 128 rows of W (one hidden tile per CTA),
+// N = the batch padded to 32, K streamed in 64-element (128 B) chunks by TMA
+// with 128-byte swizzle into a mbarrier ring; one elected thread issues
+// tcgen05.mma (kind::f16, bf16 in, fp32 accumulate in TMEM) and commits each
+// stage back to the producer.  The epilogue reads TMEM with tcgen05.ld.
+//
+// Split-K spreads the hidden tiles over every SM; the last CTA of a tile
+// (atomic ticket) sums the split partials in split order.  That CTA then
+// pushes the bf16 tile into every peer's inbox slot for this rank (P2P stores
+// over NVLink into IPC-mapped symmetric buffers), raises the tile's flag on
+// each peer (st.release.sys), waits for every rank's flag on its own copy of
+// the tile (ld.acquire.sys) and sums the world's partials in rank order - a
+// one-shot all-reduce overlapped with the GEMM tile by tile.  Every rank sums
+// the same bf16 values in the same order, so all ranks hold identical bits.
+//
+// Reuse of an inbox slot two calls later is safe with two parities: a peer
+// can only write epoch e+2 after finishing e+1, which needs this rank's e+1
+// pushes, which come after this rank finished reading epoch e (stream order).
+#include <cudaTypedefs.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/orbitflow_b200.h"
+#include "common.cuh"
+
+namespace ofb {
+int report_error(int code, const char* msg);
+int report_cuda(cudaError_t e, const char* what);
+int encode_bf16_map(CUtensorMap* map, void* base, int rank, const uint64_t* dims,
+                    const uint64_t* byte_strides, const uint32_t* box);
+
+namespace {
+
+constexpr int kTileM = 128;        // hidden rows per CTA = UMMA M = TMEM lanes
+constexpr int kChunkK = 64;        // K elements per pipeline stage (one 128 B swizzle atom)
+constexpr int kThreads = 128;      // 4 warps: TMA producer, MMA issuer, TMEM owner, all epilogue
+constexpr int kMaxPeers = 8;
+constexpr int kMaxStages = 8;
+constexpr int kSmemBudget = 200 * 1024;
+
+struct OprojArgs {
+  int layer, batch, npad, k, hidden, tiles, splits, chunks, stages;
+  int world, rank, max_batch;
+  uint32_t epoch;
+  long long timeout_ns;
+  float* part;              // fp32 [tiles][splits][npad][128]
+  unsigned int* tickets;    // [tiles]
+  __nv_bfloat16* out;       // [batch][hidden]
+  int* status;
+  char* symm[kMaxPeers];
+  long long flags_off;      // byte offset of the flags inside a symmetric buffer
+};
+
+// ---------------------------------------------------------------- tcgen05
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+               ::"r"(smem_u32(dst)), "r"(cols) : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_dealloc(uint32_t addr, uint32_t cols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(addr), "r"(cols)
+               : "memory");
+}
+
+// Shared-memory matrix descriptor: K-major operand, 128-byte swizzle, rows of
+// 128 B, 8-row groups 1024 B apart (SBO); LBO is unused for swizzled K-major.
+__device__ __forceinline__ uint64_t sw128_kmajor_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr & 0x3FFFF) >> 4);
+  d |= static_cast<uint64_t>(1) << 16;               // LBO (ignored)
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;       // SBO
+  d |= static_cast<uint64_t>(1) << 46;               // descriptor version (sm_100)
+  d |= static_cast<uint64_t>(2) << 61;               // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor, kind::f16: bf16 A/B, fp32 D, both K-major, M x N.
+__host__ __device__ constexpr uint32_t umma_idesc_bf16(int m, int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+      ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               ::"r"(smem_u32(bar)) : "memory");
+}
+
+// 32 lanes x 32 columns of fp32: thread i of the warp gets its lane's 32 columns.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];"
+      ::"r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)),
+        "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
+// ---------------------------------------------------------------- system-scope flags
+__device__ __forceinline__ void st_release_sys(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ long long globaltimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void add_bf16x8(float* acc, uint4 u) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __bfloat1622float2(h[i]);
+    acc[2 * i] += f.x;
+    acc[2 * i + 1] += f.y;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
+                       const __grid_constant__ CUtensorMap xmap,
+                       const __grid_constant__ OprojArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  __shared__ uint64_t full_bar[kMaxStages], empty_bar[kMaxStages], acc_bar;
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ int last_sh;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x / a.splits, split = blockIdx.x % a.splits;
+  const int c0 = split * a.chunks / a.splits;
+  const int nchunks = (split + 1) * a.chunks / a.splits - c0;
+  const int stage_w = kTileM * kChunkK * 2;          // 16 KiB of W rows
+  const int stage_bytes = stage_w + a.npad * kChunkK * 2;
+  const uint32_t tcols = a.npad <= 32 ? 32u : a.npad <= 64 ? 64u : a.npad <= 128 ? 128u : 256u;
+
+  if (threadIdx.x == 0) {
+    prefetch_tma_desc(&wmap);
+    prefetch_tma_desc(&xmap);
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&acc_bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(&tmem_base_sh, tcols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == 0 && lane == 0) {
+    // TMA producer: W rows [tile*128, +128) x K chunk, and the batch rows x K chunk
+    for (int i = 0; i < nchunks; ++i) {
+      const int s = i % a.stages, round = i / a.stages;
+      if (round > 0) mbar_wait(&empty_bar[s], (round - 1) & 1);
+      uint8_t* sw = smem + s * stage_bytes;
+      mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
+      tma_load_3d(sw, &wmap, &full_bar[s], (c0 + i) * kChunkK, tile * kTileM, a.layer);
+      tma_load_3d(sw + stage_w, &xmap, &full_bar[s], (c0 + i) * kChunkK, 0, a.layer);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // MMA issuer: D[128 x npad] (TMEM) += W_tile[128 x 64] . X[npad x 64]^T per stage
+    const uint32_t idesc = umma_idesc_bf16(kTileM, a.npad);
+    for (int i = 0; i < nchunks; ++i) {
+      const int s = i % a.stages, round = i / a.stages;
+      mbar_wait(&full_bar[s], round & 1);
+      tc_fence_after();
+      const uint64_t ad = sw128_kmajor_desc(smem_u32(smem + s * stage_bytes));
+      const uint64_t bd = sw128_kmajor_desc(smem_u32(smem + s * stage_bytes + stage_w));
+#pragma unroll
+      for (int k = 0; k < kChunkK / 16; ++k)   // +32 B per K=16 step inside the swizzle atom
+        umma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
+      umma_commit(&empty_bar[s]);              // frees the stage once these MMAs have read it
+    }
+    umma_commit(&acc_bar);
+  }
+  __syncwarp();
+
+  // ---- epilogue: TMEM -> registers (row m = warp*32 + lane of the tile)
+  mbar_wait(&acc_bar, 0);
+  tc_fence_after();
+  const int m = warp * 32 + lane;
+  __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(smem);   // [npad][128]; the ring is idle now
+  float* mypart = a.part + (static_cast<size_t>(tile) * a.splits + split) * a.npad * kTileM;
+  for (int c = 0; c < a.npad / 32; ++c) {
+    uint32_t v[32];
+    tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c * 32, v);
+    if (a.splits > 1) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) mypart[(c * 32 + j) * kTileM + m] = __uint_as_float(v[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) stg[(c * 32 + j) * kTileM + m] = __float2bfloat16_rn(__uint_as_float(v[j]));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc(tmem, tcols);
+
+  if (a.splits > 1) {
+    // last CTA of the tile sums the split partials in split order (deterministic)
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned int t = atomicAdd(&a.tickets[tile], 1u);
+      last_sh = (t == static_cast<unsigned int>(a.splits - 1));
+      if (last_sh) a.tickets[tile] = 0;   // re-armed for the next launch
+    }
+    __syncthreads();
+    if (!last_sh) return;
+    __threadfence();
+    const float* base = a.part + static_cast<size_t>(tile) * a.splits * a.npad * kTileM;
+    for (int b = 0; b < a.batch; ++b) {
+      float acc = 0.f;
+      for (int s = 0; s < a.splits; ++s) acc += __ldcg(base + (static_cast<size_t>(s) * a.npad + b) * kTileM + m);
+      stg[b * kTileM + m] = __float2bfloat16_rn(acc);
+    }
+    __syncthreads();
+  }
+
+  const int nvec = a.batch * (kTileM / 8);     // 16-byte vectors of the [batch][128] tile
+  const uint4* s4 = reinterpret_cast<const uint4*>(stg);
+  if (a.world == 1) {
+    for (int i = threadIdx.x; i < nvec; i += kThreads) {
+      const int b = i >> 4, o = i & 15;
+      *reinterpret_cast<uint4*>(a.out + static_cast<size_t>(b) * a.hidden + tile * kTileM + o * 8) = s4[i];
+    }
+    return;
+  }
+
+  // ---- one-shot all-reduce of this tile over peer memory
+  const int p = static_cast<int>(a.epoch & 1u);
+  const size_t slot = static_cast<size_t>(a.max_batch) * kTileM;          // elements per (src, tile)
+  const size_t src_stride = static_cast<size_t>(a.tiles) * slot;
+  const size_t mine = (static_cast<size_t>(p) * a.world + a.rank) * src_stride + tile * slot;
+  for (int r = 0; r < a.world; ++r) {
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.symm[r]) + mine);
+    for (int i = threadIdx.x; i < nvec; i += kThreads) dst[i] = s4[i];
+  }
+  __threadfence_system();
+  __syncthreads();
+  const size_t flag_idx = (static_cast<size_t>(p) * a.world + a.rank) * a.tiles + tile;
+  if (threadIdx.x < a.world)
+    st_release_sys(reinterpret_cast<unsigned int*>(a.symm[threadIdx.x] + a.flags_off) + flag_idx, a.epoch);
+  if (threadIdx.x < a.world) {
+    const unsigned int* f = reinterpret_cast<const unsigned int*>(a.symm[a.rank] + a.flags_off) +
+                            (static_cast<size_t>(p) * a.world + threadIdx.x) * a.tiles + tile;
+    const long long t0 = globaltimer();
+    while (static_cast<int>(ld_acquire_sys(f) - a.epoch) < 0) {
+      if (globaltimer() - t0 > a.timeout_ns) {
+        atomicExch(a.status, 1);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  const __nv_bfloat16* inbox = reinterpret_cast<const __nv_bfloat16*>(a.symm[a.rank]) +
+                               static_cast<size_t>(p) * a.world * src_stride + tile * slot;
+  for (int i = threadIdx.x; i < nvec; i += kThreads) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int r = 0; r < a.world; ++r)
+      add_bf16x8(acc, __ldcg(reinterpret_cast<const uint4*>(inbox + r * src_stride) + i));
+    uint4 o;
+    o.x = pack_bf16(acc[0], acc[1]);
+    o.y = pack_bf16(acc[2], acc[3]);
+    o.z = pack_bf16(acc[4], acc[5]);
+    o.w = pack_bf16(acc[6], acc[7]);
+    const int b = i >> 4, q = i & 15;
+    *reinterpret_cast<uint4*>(a.out + static_cast<size_t>(b) * a.hidden + tile * kTileM + q * 8) = o;
+  }
+}
+
+int padded_batch(int batch) { return (batch + 31) / 32 * 32; }
+
+int num_sms() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+int choose_splits(int tiles, int chunks) {
+  int s = num_sms() / tiles;
+  if (s < 1) s = 1;
+  if (s > chunks) s = chunks;
+  return s;
+}
+
+size_t inbox_bytes(int world, int max_batch, int hidden) {
+  return static_cast<size_t>(2) * world * static_cast<size_t>(hidden) * max_batch * 2;
+}
+
+size_t flags_bytes(int world, int hidden) {
+  return static_cast<size_t>(2) * world * (hidden / kTileM) * 4;
+}
+
+struct MapKey {
+  const void* x;
+  const void* w;
+  int layers, batch, k, hidden, npad;
+  CUtensorMap xmap, wmap;
+};
+std::mutex g_map_mu;
+std::vector<MapKey> g_map_cache;
+
+int get_maps(const ofb_oproj_desc* d, int npad, CUtensorMap* xmap, CUtensorMap* wmap) {
+  std::lock_guard<std::mutex> lock(g_map_mu);
+  for (auto& e : g_map_cache)
+    if (e.x == d->x && e.w == d->w && e.layers == d->layers && e.batch == d->batch &&
+        e.k == d->k && e.hidden == d->hidden && e.npad == npad) {
+      *xmap = e.xmap;
+      *wmap = e.wmap;
+      return 0;
+    }
+  MapKey e{d->x, d->w, d->layers, d->batch, d->k, d->hidden, npad, {}, {}};
+  const uint64_t row = static_cast<uint64_t>(d->k) * 2;
+  {  // X: [layers][batch][k]; box 64 x npad x 1 (rows past the batch read as zero)
+    uint64_t dims[3] = {static_cast<uint64_t>(d->k), static_cast<uint64_t>(d->batch),
+                        static_cast<uint64_t>(d->layers)};
+    uint64_t strides[2] = {row, row * d->batch};
+    uint32_t box[3] = {static_cast<uint32_t>(kChunkK), static_cast<uint32_t>(npad), 1};
+    int rc = encode_bf16_map(&e.xmap, const_cast<void*>(d->x), 3, dims, strides, box);
+    if (rc) return rc;
+  }
+  {  // W: [layers][hidden][k]; box 64 x 128 x 1
+    uint64_t dims[3] = {static_cast<uint64_t>(d->k), static_cast<uint64_t>(d->hidden),
+                        static_cast<uint64_t>(d->layers)};
+    uint64_t strides[2] = {row, row * d->hidden};
+    uint32_t box[3] = {static_cast<uint32_t>(kChunkK), static_cast<uint32_t>(kTileM), 1};
+    int rc = encode_bf16_map(&e.wmap, const_cast<void*>(d->w), 3, dims, strides, box);
+    if (rc) return rc;
+  }
+  if (g_map_cache.size() > 256) g_map_cache.erase(g_map_cache.begin());
+  g_map_cache.push_back(e);
+  *xmap = e.xmap;
+  *wmap = e.wmap;
+  return 0;
+}
+
+}  // namespace
+}  // namespace ofb
+
+extern "C" {
+
+int ofb_symm_alloc(int64_t bytes, void** ptr) {
+  if (!ptr || bytes <= 0) return ofb::report_error(-1, "ofb_symm_alloc: bad arguments");
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, static_cast<size_t>(bytes));
+  if (e != cudaSuccess) return ofb::report_cuda(e, "cudaMalloc (symmetric buffer)");
+  e = cudaMemset(p, 0, static_cast<size_t>(bytes));
+  if (e != cudaSuccess) return ofb::report_cuda(e, "cudaMemset (symmetric buffer)");
+  *ptr = p;
+  return 0;
+}
+
+int ofb_symm_free(void* ptr) {
+  if (ptr) {
+    cudaError_t e = cudaFree(ptr);
+    if (e != cudaSuccess) return ofb::report_cuda(e, "cudaFree (symmetric buffer)");
+  }
+  return 0;
+}
+
+int ofb_ipc_get_handle(void* ptr, void* handle64) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handles are 64 bytes");
+  if (!ptr || !handle64) return ofb::report_error(-1, "ofb_ipc_get_handle: null argument");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, ptr);
+  if (e != cudaSuccess) return ofb::report_cuda(e, "cudaIpcGetMemHandle");
+  memcpy(handle64, &h, sizeof(h));
+  return 0;
+}
+
+int ofb_ipc_open_handle(const void* handle64, void** ptr) {
+  if (!handle64 || !ptr) return ofb::report_error(-1, "ofb_ipc_open_handle: null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return ofb::report_cuda(e, "cudaIpcOpenMemHandle");
+  return 0;
+}
+
+int ofb_ipc_close_handle(void* ptr) {
+  if (ptr) {
+    cudaError_t e = cudaIpcCloseMemHandle(ptr);
+    if (e != cudaSuccess) return ofb::report_cuda(e, "cudaIpcCloseMemHandle");
+  }
+  return 0;
+}
+
+int64_t ofb_oproj_symm_bytes(int32_t world, int32_t max_batch, int32_t hidden) {
+  if (world < 1 || world > ofb::kMaxPeers || max_batch < 1 || hidden < ofb::kTileM) return -1;
+  const size_t inbox = (ofb::inbox_bytes(world, max_batch, hidden) + 255) / 256 * 256;
+  return static_cast<int64_t>(inbox + ofb::flags_bytes(world, hidden));
+}
+
+int64_t ofb_oproj_workspace_bytes(int32_t max_batch, int32_t k, int32_t hidden) {
+  if (max_batch < 1 || k < ofb::kChunkK || hidden < ofb::kTileM) return -1;
+  const int tiles = hidden / ofb::kTileM;
+  const int splits = ofb::choose_splits(tiles, k / ofb::kChunkK);
+  const size_t part = static_cast<size_t>(tiles) * splits * ofb::padded_batch(max_batch) * ofb::kTileM * 4;
+  return static_cast<int64_t>(part + static_cast<size_t>(tiles) * 4 + 256);
+}
+
+int ofb_oproj_allreduce(const ofb_oproj_desc* d, void* stream) {
+  using namespace ofb;
+  if (!d) return report_error(-1, "ofb_oproj_allreduce: null descriptor");
+  if (!d->x || !d->w || !d->out || !d->workspace)
+    return report_error(-1, "ofb_oproj_allreduce: null tensor");
+  if (d->batch < 1 || d->batch > d->max_batch || d->max_batch > 256)
+    return report_error(-1, "ofb_oproj_allreduce: need 1 <= batch <= max_batch <= 256");
+  if (d->k < kChunkK || d->k % kChunkK) return report_error(-1, "ofb_oproj_allreduce: k must be a multiple of 64");
+  if (d->hidden < kTileM || d->hidden % kTileM)
+    return report_error(-1, "ofb_oproj_allreduce: hidden must be a multiple of 128");
+  if (d->layer < 0 || d->layer >= d->layers) return report_error(-1, "ofb_oproj_allreduce: layer out of range");
+  if (d->world < 1 || d->world > kMaxPeers || d->rank < 0 || d->rank >= d->world)
+    return report_error(-1, "ofb_oproj_allreduce: bad world / rank");
+  if (d->world > 1) {
+    if (d->epoch == 0) return report_error(-1, "ofb_oproj_allreduce: epoch must be > 0");
+    if (!d->status) return report_error(-1, "ofb_oproj_allreduce: status pointer required");
+    for (int r = 0; r < d->world; ++r)
+      if (!d->symm[r]) return report_error(-1, "ofb_oproj_allreduce: missing peer buffer");
+  }
+  const int npad = padded_batch(d->batch);
+  const int tiles = d->hidden / kTileM;
+  const int chunks = d->k / kChunkK;
+  const int splits = choose_splits(tiles, chunks);
+  const size_t part = static_cast<size_t>(tiles) * splits * padded_batch(d->max_batch) * kTileM * 4;
+  if (static_cast<size_t>(d->workspace_bytes) < part + static_cast<size_t>(tiles) * 4)
+    return report_error(-1, "ofb_oproj_allreduce: workspace too small (ofb_oproj_workspace_bytes)");
+  CUtensorMap xmap, wmap;
+  int rc = get_maps(d, npad, &xmap, &wmap);
+  if (rc) return rc;
+
+  OprojArgs a{};
+  a.layer = d->layer;
+  a.batch = d->batch;
+  a.npad = npad;
+  a.k = d->k;
+  a.hidden = d->hidden;
+  a.tiles = tiles;
+  a.splits = splits;
+  a.chunks = chunks;
+  const int stage_bytes = kTileM * kChunkK * 2 + npad * kChunkK * 2;
+  a.stages = std::max(2, std::min(kMaxStages, kSmemBudget / stage_bytes));
+  a.world = d->world;
+  a.rank = d->rank;
+  a.max_batch = d->max_batch;
+  a.epoch = d->epoch;
+  a.timeout_ns = d->timeout_ns > 0 ? d->timeout_ns : 5000000000LL;
+  a.part = static_cast<float*>(d->workspace);
+  a.tickets = reinterpret_cast<unsigned int*>(static_cast<char*>(d->workspace) + part);
+  a.out = static_cast<__nv_bfloat16*>(d->out);
+  a.status = d->status;
+  for (int r = 0; r < d->world; ++r) a.symm[r] = static_cast<char*>(d->symm[r]);
+  a.flags_off = static_cast<long long>((inbox_bytes(d->world, d->max_batch, d->hidden) + 255) / 256 * 256);
+
+  const size_t smem = static_cast<size_t>(a.stages) * stage_bytes + 1024;
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(oproj_allreduce_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kSmemBudget + 2048));
+    if (e != cudaSuccess) return report_cuda(e, "cudaFuncSetAttribute(oproj_allreduce_kernel)");
+    configured = kSmemBudget + 2048;
+  }
+  oproj_allreduce_kernel<<<tiles * splits, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(wmap, xmap, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return report_cuda(e, "oproj_allreduce_kernel launch");
+  return 0;
+}
+
+}  // extern "C"

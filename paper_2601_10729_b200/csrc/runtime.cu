@@ -116,6 +116,28 @@ int get_kv_map(void* pool, int64_t pool_blocks, int hkv, CUtensorMap* out) {
 
 }  // namespace
 
+// Helpers shared with the other translation units (oproj_allreduce.cu).
+namespace ofb {
+int report_error(int code, const char* msg) { return fail(code, msg); }
+int report_cuda(cudaError_t e, const char* what) { return cuda_fail(e, what); }
+
+// bf16 tensor map with 128-byte swizzle and zero fill out of bounds.
+int encode_bf16_map(CUtensorMap* map, void* base, int rank, const uint64_t* dims,
+                    const uint64_t* byte_strides, const uint32_t* box) {
+  int rc = load_encoder();
+  if (rc) return rc;
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, base,
+                        reinterpret_cast<const cuuint64_t*>(dims),
+                        reinterpret_cast<const cuuint64_t*>(byte_strides),
+                        reinterpret_cast<const cuuint32_t*>(box), estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(-1, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return 0;
+}
+}  // namespace ofb
+
 // ------------------------------------------------------------------ runtime
 
 struct CopyTiming {
