@@ -369,7 +369,7 @@ def run_ours(args, cfg):
 
     attn_tokens = []
 
-    tpd = TensorParallelDecoder(ex, shard, cfg["hidden"], seed=0) if use_tp else None
+    tpd = TensorParallelDecoder(ex, shard, cfg["hidden"], seed=0, max_batch=B) if use_tp else None
 
     def run_step(inp):
         if tpd is not None:
@@ -480,9 +480,10 @@ def run_ours(args, cfg):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) KV, q)",
         "config": {"workload": cfg["workload"], "global_batch": B, "seq_len": cfg["prompt"],
                    "layers": L, "q_heads": hq_total, "kv_heads": hkv_total,
-                   "parallelism": (f"tp{world} (KV-head sharded, o-proj all-reduce per layer)"
+                   "parallelism": (f"tp{world} (KV-head sharded; per layer K6: tcgen05 o-proj "
+                                   f"fused with a one-shot all-reduce over NVLink peer memory)"
                                    if world > 1 else
-                                   f"tp{tp} rank-0 shard emulated on 1 GPU (no collective)"
+                                   f"tp{tp} rank-0 shard emulated on 1 GPU (K6 o-proj, no exchange)"
                                    if tp > 1 else "single GPU"),
                    "placement_rows_offloaded": [row.count(0) for row in placement.rows][:4],
                    "offloaded_slabs": n_off, "staging_slots": slots,
@@ -516,13 +517,16 @@ def run_ours(args, cfg):
                           "blocks_to_fetch_check": blocks_to_fetch(placement, batch)},
         "attn_share_of_step": tm["acc_attn_ms"] / max(tm["acc_step_ms"], 1e-9),
         "gpu_launches": args.steps * (1 + L + len({l for row in placement.rows
-                                                   for l, b in enumerate(row) if b == 0})),
+                                                   for l, b in enumerate(row) if b == 0})
+                                      + (L if tpd is not None else 0)),
         "clocks": clocks.summary(),
     }
     if cpu is not None:
         line["cpu_baseline"] = cpu
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if tpd is not None:
+        tpd.close()
     ex.close()
     if dist is not None:
         dist.destroy_process_group()

@@ -54,6 +54,7 @@ class SymmetricBuffers:
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._opened: list[int] = []
         self._owned = _owned
+        self._group = group
         lib = _lib()
         self._emulated = _peers is not None
         if _peers is not None:           # emulated group: pointers supplied by the factory
@@ -110,8 +111,14 @@ class SymmetricBuffers:
             raise RuntimeError(f"rank {self.rank}: a peer's tile never arrived (C1 exchange timed out)")
 
     def close(self) -> None:
+        """Collective when world > 1: no rank frees its buffer while a peer may
+        still be writing into it."""
         lib = _lib()
         torch.cuda.synchronize(self.device)
+        if self._opened:
+            import torch.distributed as dist
+
+            dist.barrier(group=self._group)
         for p in self._opened:
             lib.ofb_ipc_close_handle(p)
         self._opened.clear()

@@ -10,8 +10,9 @@
 // tcgen05.mma (kind::f16, bf16 in, fp32 accumulate in TMEM) and commits each
 // stage back to the producer.  The epilogue reads TMEM with tcgen05.ld.
 //
-// Split-K spreads the hidden tiles over every SM; the last CTA of a tile
-// (atomic ticket) sums the split partials in split order.  That CTA then
+// Split-K spreads the hidden tiles over every SM: the CTAs of one tile form a
+// thread-block cluster, the non-leaders ship their fp32 partial into the
+// leader's shared memory (DSMEM) and the leader sums in split order.  It then
 // pushes the bf16 tile into every peer's inbox slot for this rank (P2P stores
 // over NVLink into IPC-mapped symmetric buffers), raises the tile's flag on
 // each peer (st.release.sys), waits for every rank's flag on its own copy of
@@ -44,15 +45,13 @@ constexpr int kChunkK = 64;        // K elements per pipeline stage (one 128 B s
 constexpr int kThreads = 128;      // 4 warps: TMA producer, MMA issuer, TMEM owner, all epilogue
 constexpr int kMaxPeers = 8;
 constexpr int kMaxStages = 8;
-constexpr int kSmemBudget = 200 * 1024;
+constexpr int kSmemBudget = 200 * 1024;   // one CTA per SM, deepest ring
 
 struct OprojArgs {
   int layer, batch, npad, k, hidden, tiles, splits, chunks, stages;
   int world, rank, max_batch;
   uint32_t epoch;
   long long timeout_ns;
-  float* part;              // fp32 [tiles][splits][npad][128]
-  unsigned int* tickets;    // [tiles]
   __nv_bfloat16* out;       // [batch][hidden]
   int* status;
   char* symm[kMaxPeers];
@@ -160,19 +159,36 @@ __device__ __forceinline__ void add_bf16x8(float* acc, uint4 u) {
   }
 }
 
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t map_to_cta(uint32_t saddr, uint32_t cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(cta));
+  return r;
+}
+
+__device__ __forceinline__ void st_cluster_f32(uint32_t addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+
+// Grid = tiles x splits, cluster = (splits, 1, 1): the CTAs of a cluster share
+// one hidden tile and split its K range; non-leaders ship their fp32 partial
+// into the leader's shared memory (DSMEM) and the leader sums in split order.
 __global__ void __launch_bounds__(kThreads, 1)
 oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
                        const __grid_constant__ CUtensorMap xmap,
                        const __grid_constant__ OprojArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  // 1024-byte aligned for the 128-byte swizzle; derived from smem_raw by an
+  // offset so the compiler keeps the shared address space (STS, not ST.E)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t full_bar[kMaxStages], empty_bar[kMaxStages], acc_bar;
   __shared__ uint32_t tmem_base_sh;
-  __shared__ int last_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x / a.splits, split = blockIdx.x % a.splits;
+  const int tile = blockIdx.x / a.splits, split = blockIdx.x % a.splits;   // split = rank in cluster
   const int c0 = split * a.chunks / a.splits;
   const int nchunks = (split + 1) * a.chunks / a.splits - c0;
   const int stage_w = kTileM * kChunkK * 2;          // 16 KiB of W rows
@@ -196,10 +212,20 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
   const uint32_t tmem = tmem_base_sh;
 
   if (warp == 0 && lane == 0) {
-    // TMA producer: W rows [tile*128, +128) x K chunk, and the batch rows x K chunk
-    for (int i = 0; i < nchunks; ++i) {
+    // TMA producer.  W_o does not depend on the previous kernel (attention), so
+    // the first ring's worth of weight tiles is requested before the
+    // programmatic-dependent-launch wait; x (the attention output) after it.
+    const int pre = nchunks < a.stages ? nchunks : a.stages;
+    for (int i = 0; i < pre; ++i) {
+      mbar_arrive_expect_tx(&full_bar[i], stage_bytes);
+      tma_load_3d(smem + i * stage_bytes, &wmap, &full_bar[i], (c0 + i) * kChunkK, tile * kTileM, a.layer);
+    }
+    pdl_wait();
+    for (int i = 0; i < pre; ++i)
+      tma_load_3d(smem + i * stage_bytes + stage_w, &xmap, &full_bar[i], (c0 + i) * kChunkK, 0, a.layer);
+    for (int i = pre; i < nchunks; ++i) {
       const int s = i % a.stages, round = i / a.stages;
-      if (round > 0) mbar_wait(&empty_bar[s], (round - 1) & 1);
+      mbar_wait(&empty_bar[s], (round - 1) & 1);
       uint8_t* sw = smem + s * stage_bytes;
       mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
       tma_load_3d(sw, &wmap, &full_bar[s], (c0 + i) * kChunkK, tile * kTileM, a.layer);
@@ -223,47 +249,52 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
   }
   __syncwarp();
 
-  // ---- epilogue: TMEM -> registers (row m = warp*32 + lane of the tile)
+  // ---- epilogue (row m = warp*32 + lane of the tile)
   mbar_wait(&acc_bar, 0);
   tc_fence_after();
+  pdl_wait();                       // every thread: the predecessor's writes are visible
+  pdl_trigger();                    // the next kernel may start its own prologue
   const int m = warp * 32 + lane;
-  __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(smem);   // [npad][128]; the ring is idle now
-  float* mypart = a.part + (static_cast<size_t>(tile) * a.splits + split) * a.npad * kTileM;
+  const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+  // leader smem (the ring is idle once every MMA of the cluster completed):
+  //   red [splits-1][npad][128] fp32 | stg [npad][128] bf16
+  float* red = reinterpret_cast<float*>(smem);
+  __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(smem + static_cast<size_t>(a.splits - 1) * a.npad * kTileM * 4);
+  if (a.splits > 1) {
+    cluster_sync_all();             // every CTA of the cluster is past its MMAs
+    if (split != 0) {
+      const uint32_t dst = map_to_cta(smem_u32(red + static_cast<size_t>(split - 1) * a.npad * kTileM), 0);
+      for (int c = 0; c < a.npad / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(trow + c * 32, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) st_cluster_f32(dst + ((c * 32 + j) * kTileM + m) * 4, __uint_as_float(v[j]));
+      }
+      tc_fence_before();
+      __syncthreads();
+      if (warp == 2) tmem_dealloc(tmem, tcols);
+      cluster_sync_all();           // partials visible in the leader
+      return;
+    }
+    cluster_sync_all();
+  }
   for (int c = 0; c < a.npad / 32; ++c) {
     uint32_t v[32];
-    tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c * 32, v);
-    if (a.splits > 1) {
+    tmem_ld32(trow + c * 32, v);
+    float acc[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) mypart[(c * 32 + j) * kTileM + m] = __uint_as_float(v[j]);
-    } else {
+    for (int j = 0; j < 32; ++j) acc[j] = __uint_as_float(v[j]);
+    for (int s = 1; s < a.splits; ++s) {       // split order: deterministic
+      const float* src = red + (static_cast<size_t>(s - 1) * a.npad + c * 32) * kTileM + m;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) stg[(c * 32 + j) * kTileM + m] = __float2bfloat16_rn(__uint_as_float(v[j]));
+      for (int j = 0; j < 32; ++j) acc[j] += src[j * kTileM];
     }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) stg[(c * 32 + j) * kTileM + m] = __float2bfloat16_rn(acc[j]);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_dealloc(tmem, tcols);
-
-  if (a.splits > 1) {
-    // last CTA of the tile sums the split partials in split order (deterministic)
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const unsigned int t = atomicAdd(&a.tickets[tile], 1u);
-      last_sh = (t == static_cast<unsigned int>(a.splits - 1));
-      if (last_sh) a.tickets[tile] = 0;   // re-armed for the next launch
-    }
-    __syncthreads();
-    if (!last_sh) return;
-    __threadfence();
-    const float* base = a.part + static_cast<size_t>(tile) * a.splits * a.npad * kTileM;
-    for (int b = 0; b < a.batch; ++b) {
-      float acc = 0.f;
-      for (int s = 0; s < a.splits; ++s) acc += __ldcg(base + (static_cast<size_t>(s) * a.npad + b) * kTileM + m);
-      stg[b * kTileM + m] = __float2bfloat16_rn(acc);
-    }
-    __syncthreads();
-  }
 
   const int nvec = a.batch * (kTileM / 8);     // 16-byte vectors of the [batch][128] tile
   const uint4* s4 = reinterpret_cast<const uint4*>(stg);
@@ -304,17 +335,36 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
   __syncthreads();
   const __nv_bfloat16* inbox = reinterpret_cast<const __nv_bfloat16*>(a.symm[a.rank]) +
                                static_cast<size_t>(p) * a.world * src_stride + tile * slot;
-  for (int i = threadIdx.x; i < nvec; i += kThreads) {
-    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int r = 0; r < a.world; ++r)
-      add_bf16x8(acc, __ldcg(reinterpret_cast<const uint4*>(inbox + r * src_stride) + i));
-    uint4 o;
-    o.x = pack_bf16(acc[0], acc[1]);
-    o.y = pack_bf16(acc[2], acc[3]);
-    o.z = pack_bf16(acc[4], acc[5]);
-    o.w = pack_bf16(acc[6], acc[7]);
-    const int b = i >> 4, q = i & 15;
-    *reinterpret_cast<uint4*>(a.out + static_cast<size_t>(b) * a.hidden + tile * kTileM + q * 8) = o;
+  constexpr int kUnroll = 4;   // vectors per thread whose loads are all issued before any store
+  for (int i0 = threadIdx.x; i0 < nvec; i0 += kThreads * kUnroll) {
+    float acc[kUnroll][8];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[u][e] = 0.f;
+    for (int r = 0; r < a.world; ++r) {         // rank order: identical sums on every rank
+      const uint4* src = reinterpret_cast<const uint4*>(inbox + r * src_stride);
+      uint4 t[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int i = i0 + u * kThreads;
+        t[u] = i < nvec ? __ldcg(src + i) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) add_bf16x8(acc[u], t[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int i = i0 + u * kThreads;
+      if (i >= nvec) break;
+      uint4 o;
+      o.x = pack_bf16(acc[u][0], acc[u][1]);
+      o.y = pack_bf16(acc[u][2], acc[u][3]);
+      o.z = pack_bf16(acc[u][4], acc[u][5]);
+      o.w = pack_bf16(acc[u][6], acc[u][7]);
+      const int b = i >> 4, q = i & 15;
+      *reinterpret_cast<uint4*>(a.out + static_cast<size_t>(b) * a.hidden + tile * kTileM + q * 8) = o;
+    }
   }
 }
 
@@ -331,10 +381,21 @@ int num_sms() {
   return sms;
 }
 
-int choose_splits(int tiles, int chunks) {
+int ring_stages(int npad) {
+  const int stage_bytes = kTileM * kChunkK * 2 + npad * kChunkK * 2;
+  return std::max(2, std::min(kMaxStages, kSmemBudget / stage_bytes));
+}
+
+// CTAs per hidden tile (= cluster size): enough to cover the SMs, at most 8
+// (portable cluster), at most one K chunk each, and the leader's reduction
+// buffers + bf16 staging must fit in its (idle) ring.
+int choose_splits(int tiles, int chunks, int npad) {
+  const size_t ring = static_cast<size_t>(ring_stages(npad)) *
+                      (kTileM * kChunkK * 2 + npad * kChunkK * 2);
   int s = num_sms() / tiles;
-  if (s < 1) s = 1;
-  if (s > chunks) s = chunks;
+  s = std::max(1, std::min(s, std::min(8, chunks)));
+  while (s > 1 && static_cast<size_t>(s - 1) * npad * kTileM * 4 + static_cast<size_t>(npad) * kTileM * 2 > ring)
+    --s;
   return s;
 }
 
@@ -448,16 +509,13 @@ int64_t ofb_oproj_symm_bytes(int32_t world, int32_t max_batch, int32_t hidden) {
 
 int64_t ofb_oproj_workspace_bytes(int32_t max_batch, int32_t k, int32_t hidden) {
   if (max_batch < 1 || k < ofb::kChunkK || hidden < ofb::kTileM) return -1;
-  const int tiles = hidden / ofb::kTileM;
-  const int splits = ofb::choose_splits(tiles, k / ofb::kChunkK);
-  const size_t part = static_cast<size_t>(tiles) * splits * ofb::padded_batch(max_batch) * ofb::kTileM * 4;
-  return static_cast<int64_t>(part + static_cast<size_t>(tiles) * 4 + 256);
+  return 256;   // reserved: split-K partials are reduced on chip (cluster DSMEM)
 }
 
 int ofb_oproj_allreduce(const ofb_oproj_desc* d, void* stream) {
   using namespace ofb;
   if (!d) return report_error(-1, "ofb_oproj_allreduce: null descriptor");
-  if (!d->x || !d->w || !d->out || !d->workspace)
+  if (!d->x || !d->w || !d->out)
     return report_error(-1, "ofb_oproj_allreduce: null tensor");
   if (d->batch < 1 || d->batch > d->max_batch || d->max_batch > 256)
     return report_error(-1, "ofb_oproj_allreduce: need 1 <= batch <= max_batch <= 256");
@@ -476,10 +534,7 @@ int ofb_oproj_allreduce(const ofb_oproj_desc* d, void* stream) {
   const int npad = padded_batch(d->batch);
   const int tiles = d->hidden / kTileM;
   const int chunks = d->k / kChunkK;
-  const int splits = choose_splits(tiles, chunks);
-  const size_t part = static_cast<size_t>(tiles) * splits * padded_batch(d->max_batch) * kTileM * 4;
-  if (static_cast<size_t>(d->workspace_bytes) < part + static_cast<size_t>(tiles) * 4)
-    return report_error(-1, "ofb_oproj_allreduce: workspace too small (ofb_oproj_workspace_bytes)");
+  const int splits = choose_splits(tiles, chunks, npad);
   CUtensorMap xmap, wmap;
   int rc = get_maps(d, npad, &xmap, &wmap);
   if (rc) return rc;
@@ -494,14 +549,12 @@ int ofb_oproj_allreduce(const ofb_oproj_desc* d, void* stream) {
   a.splits = splits;
   a.chunks = chunks;
   const int stage_bytes = kTileM * kChunkK * 2 + npad * kChunkK * 2;
-  a.stages = std::max(2, std::min(kMaxStages, kSmemBudget / stage_bytes));
+  a.stages = ring_stages(npad);
   a.world = d->world;
   a.rank = d->rank;
   a.max_batch = d->max_batch;
   a.epoch = d->epoch;
   a.timeout_ns = d->timeout_ns > 0 ? d->timeout_ns : 5000000000LL;
-  a.part = static_cast<float*>(d->workspace);
-  a.tickets = reinterpret_cast<unsigned int*>(static_cast<char*>(d->workspace) + part);
   a.out = static_cast<__nv_bfloat16*>(d->out);
   a.status = d->status;
   for (int r = 0; r < d->world; ++r) a.symm[r] = static_cast<char*>(d->symm[r]);
@@ -516,8 +569,22 @@ int ofb_oproj_allreduce(const ofb_oproj_desc* d, void* stream) {
     if (e != cudaSuccess) return report_cuda(e, "cudaFuncSetAttribute(oproj_allreduce_kernel)");
     configured = kSmemBudget + 2048;
   }
-  oproj_allreduce_kernel<<<tiles * splits, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(wmap, xmap, a);
-  cudaError_t e = cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(tiles * splits);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = splits;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  // W_o prefetch overlaps the attention kernel's tail (the x loads wait)
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, oproj_allreduce_kernel, wmap, xmap, a);
   if (e != cudaSuccess) return report_cuda(e, "oproj_allreduce_kernel launch");
   return 0;
 }

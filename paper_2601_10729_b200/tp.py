@@ -11,8 +11,10 @@ pure functions of the batch, so every rank recomputes the identical
 placement (C2) - ``check_plan_replicated`` verifies it with one tiny
 all-gather instead of broadcasting B x L bits every step.
 
-Works on NCCL (GPU ranks) and gloo (CPU tests) alike: the collective is
-``torch.distributed``; the attention itself is the executor's native step.
+On the GPU the exchange is K6 (``collective.py``: tcgen05 projection fused
+with a one-shot all-reduce over IPC peer memory); ``oproj_allreduce`` below is
+the same C1 written with ``torch.distributed`` - the formulation the gloo
+host-logic tests check and the plain reference the kernel is compared with.
 """
 
 from __future__ import annotations
@@ -95,25 +97,43 @@ def check_plan_replicated(rows, group=None) -> bool:
 
 class TensorParallelDecoder:
     """One rank of a KV-head-sharded decode step: the executor's native step
-    split per layer, each layer followed by o-projection + all-reduce (C1) on
-    the same stream, so layer l+1 is ordered after layer l's exchange - the
-    dependency a real decoder has (q of l+1 derives from hidden of l)."""
+    split per layer, each layer followed by the fused o-projection + all-reduce
+    (K6, ``collective.OprojAllReduce``) on the same stream, so layer l+1 is
+    ordered after layer l's exchange - the dependency a real decoder has (q of
+    l+1 derives from hidden of l).  With ``torch.distributed`` initialised and
+    world > 1 the ranks exchange CUDA IPC handles once and the kernel pushes
+    its tiles straight into the peers' memory; otherwise it is the projection
+    alone (a TP-N shard emulated on one GPU)."""
 
-    def __init__(self, executor, shard: HeadShard, hidden: int, group=None, seed: int = 0):
+    def __init__(self, executor, shard: HeadShard, hidden: int, group=None, seed: int = 0,
+                 max_batch: int = 256):
+        import torch.distributed as dist
+
+        from .collective import OprojAllReduce, SymmetricBuffers
+
         self.ex = executor
         self.shard = shard
         self.hidden = hidden
         self.group = group
         L = executor.shape.num_layers
         g = torch.Generator(device=executor.device)
-        g.manual_seed(1234 + seed)   # identical full W_o on every rank; each keeps its rows
-        rows = shard.local_q * 128
-        full_rows = shard.num_q_heads * 128
-        scale = full_rows ** -0.5
-        self.w_o = torch.empty((L, rows, hidden), dtype=torch.bfloat16, device=executor.device)
+        g.manual_seed(1234 + seed)   # identical full W_o on every rank; each keeps its columns
+        full_k = shard.num_q_heads * 128
+        lo, hi = shard.q_heads.start * 128, shard.q_heads.stop * 128
+        scale = full_k ** -0.5
+        # nn.Linear layout [hidden, Hq*128]; this rank multiplies its heads' columns
+        self.w_o = torch.empty((L, hidden, hi - lo), dtype=torch.bfloat16, device=executor.device)
         for l in range(L):
-            w = torch.randn((full_rows, hidden), generator=g, device=executor.device) * scale
-            self.w_o[l] = w[shard.q_heads.start * 128: shard.q_heads.stop * 128].to(torch.bfloat16)
+            w = torch.randn((hidden, full_k), generator=g, device=executor.device) * scale
+            self.w_o[l] = w[:, lo:hi].to(torch.bfloat16)
+        world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+        self.symm = None
+        if world > 1:
+            if world != shard.world:
+                raise ValueError("process group size differs from the head shard's world")
+            self.symm = SymmetricBuffers(world, shard.rank, max_batch, hidden, group=group,
+                                         device=executor.device)
+        self.proj = OprojAllReduce(self.w_o, max_batch, self.symm)
         self.last_hidden = None
 
     def step(self, batch, inputs=None) -> torch.Tensor:
@@ -127,7 +147,7 @@ class TensorParallelDecoder:
         try:
             for l in range(L):
                 ex.runtime.step_layers(1)
-                hidden[l] = oproj_allreduce(out[l], self.w_o[l], self.group)
+                self.proj(out, l, out=hidden[l], stream=stream)
         finally:
             ex.runtime.step_end()
         done = torch.cuda.Event()
@@ -139,3 +159,9 @@ class TensorParallelDecoder:
             ex._inflight.popleft()[0].synchronize()
         self.last_hidden = hidden
         return hidden
+
+    def close(self) -> None:
+        if self.symm is not None:
+            self.symm.check()
+            self.symm.close()
+            self.symm = None

@@ -197,7 +197,7 @@ def test_tensor_parallel_split_step_matches_fused_step():
             tpd = TensorParallelDecoder(ex, HeadShard(0, 1, 8, 2), hidden=256, seed=1)
             hidden = tpd.step(batch, inp)
             ex.drain()
-            want = torch.einsum("lbk,lkh->lbh", ex.last_output.reshape(4, 3, -1).float(),
+            want = torch.einsum("lbk,lhk->lbh", ex.last_output.reshape(4, 3, -1).float(),
                                 tpd.w_o.float())
             torch.testing.assert_close(hidden.float(), want, rtol=2e-2, atol=2e-2)
         else:
