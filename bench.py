@@ -421,7 +421,7 @@ def run_ours(args, cfg):
     step(0, e2e=True)
     barrier()
     e0 = time.perf_counter()
-    e2e_steps = max(3, args.steps)
+    e2e_steps = max(8, args.steps)
     for i in range(e2e_steps):
         step(i, e2e=True)
     barrier()
