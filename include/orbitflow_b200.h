@@ -44,6 +44,10 @@ OFB_API const char* ofb_last_error(void);
  * splits + last-CTA combine, 2 = auto (default: stream-K unless few (request,
  * kv head) pairs span the whole grid).  Returns the previous variant. */
 OFB_API int ofb_set_attention_kernel(int32_t variant);
+/* Diagnostics: stream-K K1 launches write 6 globaltimer stamps per CTA (entry,
+ * past the dependency wait, first tile ready, last tile consumed, exit, SM id)
+ * into `device_buffer` (uint64 [448][6]); NULL switches tracing off. */
+OFB_API int ofb_k1_trace(void* device_buffer);
 /* SM count and resident attention CTAs per SM on the current device. */
 OFB_API int ofb_device_info(int32_t* num_sms, int32_t* attn_ctas_per_sm);
 

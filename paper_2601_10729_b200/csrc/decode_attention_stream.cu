@@ -42,7 +42,18 @@ struct StreamArgs {
   int32_t* counters;  // [B * Hkv], zero at rest
   int max_blocks, batch, hq, hkv, group, grid;
   float scale_log2;
+  unsigned long long* trace;  // diagnostics (ofb_k1_trace): per CTA globaltimer stamps, or null
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// trace slots per CTA: entry, past pdl_wait, first tile ready, last tile
+// consumed, exit, SM id
+constexpr int kTraceSlots = 6;
 
 __device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
@@ -82,6 +93,13 @@ paged_gqa_decode_stream_kernel(const __grid_constant__ CUtensorMap kv_map, const
   const int cta = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = a.group;
+  unsigned long long* tr = (a.trace && tid == 0) ? a.trace + (size_t)cta * kTraceSlots : nullptr;
+  if (tr) {
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    tr[0] = gtimer();
+    tr[5] = smid;
+  }
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -122,6 +140,7 @@ paged_gqa_decode_stream_kernel(const __grid_constant__ CUtensorMap kv_map, const
   // the previous layer's K1 sharing this workspace) must be complete past here.
   pdl_wait();
   pdl_trigger();
+  if (tr) tr[1] = gtimer();
 
   // Effective grid: the host sized it for max_seq_len; with shorter actual
   // sequences keep >= 1 tile per CTA so no CTA range is empty (ticket counts
@@ -201,6 +220,10 @@ paged_gqa_decode_stream_kernel(const __grid_constant__ CUtensorMap kv_map, const
     for (; e < e_hi; e += kSConsumers) {
       const int s = e % kSStages;
       mbar_wait(&full[s], (e / kSStages) & 1);
+      if (tr) {
+        if (e == 0) tr[2] = gtimer();
+        if (e + kSConsumers >= n) tr[3] = gtimer();
+      }
       const int lb = (int)(begin + e - pb);
       const int valid = min(kBlockTokens, seq - lb * kBlockTokens);
       attend_tile(st, qa, ring + (size_t)s * kHeadBlockBytes, valid, a.scale_log2, lane);
@@ -271,12 +294,23 @@ paged_gqa_decode_stream_kernel(const __grid_constant__ CUtensorMap kv_map, const
         float acc[kMaxGroup];
 #pragma unroll
         for (int row = 0; row < kMaxGroup; ++row) acc[row] = 0.f;
-#pragma unroll 2
-        for (int k = 0; k < nseg; ++k) {
-          const float* src = a.ws_o + (size_t)seg_off[k] * kHeadDim + d;
+        // 4 segments x g rows of loads in flight before any FMA (latency-bound tail)
+        for (int k0 = 0; k0 < nseg; k0 += 4) {
+          float v[4][kMaxGroup];
 #pragma unroll
-          for (int row = 0; row < kMaxGroup; ++row)
-            if (row < g) acc[row] += wts[row * kSMaxGrid + k] * __ldcg(src + row * kHeadDim);
+          for (int u = 0; u < 4; ++u) {
+            const int k = k0 + u < nseg ? k0 + u : nseg - 1;
+            const float* src = a.ws_o + (size_t)seg_off[k] * kHeadDim + d;
+#pragma unroll
+            for (int row = 0; row < kMaxGroup; ++row) v[u][row] = row < g ? __ldcg(src + row * kHeadDim) : 0.f;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (k0 + u >= nseg) break;
+#pragma unroll
+            for (int row = 0; row < kMaxGroup; ++row)
+              if (row < g) acc[row] += wts[row * kSMaxGrid + k0 + u] * v[u][row];
+          }
         }
 #pragma unroll
         for (int row = 0; row < kMaxGroup; ++row)
@@ -287,9 +321,14 @@ paged_gqa_decode_stream_kernel(const __grid_constant__ CUtensorMap kv_map, const
     consumer_bar();  // merge scratch is reused by the next pair
     x = seg_end;
   }
+  if (tr) tr[4] = gtimer();
 }
 
 // ------------------------------------------------------------------ host side
+
+static unsigned long long* g_k1_trace = nullptr;
+unsigned long long* k1_trace_buffer() { return g_k1_trace; }
+void set_k1_trace_buffer(void* buf) { g_k1_trace = static_cast<unsigned long long*>(buf); }
 
 static int g_stream_occ = 0, g_stream_sms = 0;
 
@@ -359,6 +398,7 @@ cudaError_t launch_decode_attention_stream(const CUtensorMap& map, const void* q
   a.ws_lse = reinterpret_cast<float*>(ws + kSCounterBytes);
   a.ws_o = reinterpret_cast<float*>(ws + kSCounterBytes +
                                     (size_t)kSMaxGrid * 2 * kMaxGroup * sizeof(float));
+  a.trace = k1_trace_buffer();
   a.max_blocks = max_blocks;
   a.batch = batch;
   a.hq = hq;

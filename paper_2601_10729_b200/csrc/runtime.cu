@@ -32,6 +32,7 @@ cudaError_t launch_kv_append(const void* k_new, const void* v_new, void* pool,
                              cudaStream_t stream);
 int attention_occupancy();
 int set_attention_variant(int variant);
+void set_k1_trace_buffer(void* buf);
 cudaError_t launch_kv_prefill(const void* k, const void* v, const uint64_t* dst, int num_layers,
                               int tokens, int hkv, cudaStream_t stream);
 }  // namespace ofb
@@ -298,6 +299,11 @@ const char* ofb_last_error(void) { return g_err.c_str(); }
 int ofb_set_attention_kernel(int32_t variant) {
   if (variant < 0 || variant > 2) return fail(-1, "variant must be 0 (stream-K), 1 (split) or 2 (auto)");
   return ofb::set_attention_variant(variant);
+}
+
+int ofb_k1_trace(void* device_buffer) {
+  ofb::set_k1_trace_buffer(device_buffer);
+  return 0;
 }
 
 int ofb_device_info(int32_t* num_sms, int32_t* attn_ctas_per_sm) {
