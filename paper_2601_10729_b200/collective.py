@@ -143,7 +143,8 @@ class OprojAllReduce:
     rank (the projection alone, no exchange).
     """
 
-    def __init__(self, w_o: torch.Tensor, max_batch: int, symm: SymmetricBuffers | None = None):
+    def __init__(self, w_o: torch.Tensor, max_batch: int, symm: SymmetricBuffers | None = None,
+                 timeout_ns: int = 0):
         if not w_o.is_cuda or w_o.dtype != torch.bfloat16 or w_o.dim() != 3:
             raise ValueError("w_o must be a bf16 CUDA tensor [layers, hidden, k]")
         self.w = w_o.contiguous()
@@ -154,6 +155,7 @@ class OprojAllReduce:
             raise ValueError("symmetric buffers sized for another hidden / batch")
         self.max_batch = max_batch
         self.symm = symm
+        self.timeout_ns = int(timeout_ns)   # per tile wait; 0 = the library default (5 s)
         lib = _lib()
         nbytes = int(lib.ofb_oproj_workspace_bytes(max_batch, self.k, self.hidden))
         self.ws = torch.zeros(nbytes, dtype=torch.uint8, device=self.w.device)
@@ -180,7 +182,7 @@ class OprojAllReduce:
         d.workspace, d.workspace_bytes = self.ws.data_ptr(), self.ws.numel()
         d.max_batch = self.max_batch
         d.status = self._status.data_ptr()
-        d.timeout_ns = 0
+        d.timeout_ns = self.timeout_ns
         if self.symm is None or self.symm.world == 1:
             d.world, d.rank, d.epoch = 1, 0, 1
             if self.symm is not None:

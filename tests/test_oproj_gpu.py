@@ -91,6 +91,25 @@ def test_emulated_ranks_all_reduce(world, b, k, h):
         bufs[0].close()
 
 
+def test_missing_peer_times_out_and_is_reported():
+    """A rank whose peer never launches must not hang the GPU: the tile wait is
+    bounded, the status word is raised and check() turns it into an error."""
+    from paper_2601_10729_b200.collective import OprojAllReduce, SymmetricBuffers
+
+    dev = torch.device("cuda:0")
+    b, k, h = 8, 128, 256
+    bufs = SymmetricBuffers.emulated(2, b, h, device=dev)
+    try:
+        xs, ws = _inputs(2, 1, b, k, h, seed=5)
+        op = OprojAllReduce(ws[0].to(dev), b, bufs[0], timeout_ns=20_000_000)
+        op(xs[0].to(dev), 0)          # rank 1 never runs
+        torch.cuda.synchronize()
+        with pytest.raises(RuntimeError, match="never arrived"):
+            bufs[0].check()
+    finally:
+        bufs[0].close()
+
+
 def _ipc_worker(rank, world, port, b, k, h, q):
     import torch.distributed as dist
 

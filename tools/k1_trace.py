@@ -22,6 +22,7 @@ ap.add_argument("--batch", type=int, default=32)
 ap.add_argument("--hq", type=int, default=8)
 ap.add_argument("--hkv", type=int, default=1)
 ap.add_argument("--seq", type=int, default=65536)
+ap.add_argument("--dump", action="store_true")
 a = ap.parse_args()
 
 dev = torch.device("cuda:0")
@@ -68,4 +69,24 @@ res["per_cta_GBps"] = [float(per_cta.min()), float(np.median(per_cta)), float(pe
 slow = np.argsort(-last)[:8]
 res["slowest_ctas"] = [{"cta": int(i), "sm": int(t[i, 5]), "last_tile_us": float(last[i]),
                         "first_us": float(first[i])} for i in slow]
+# per SM: are the two co-resident CTAs slow together (SM-level) or split unevenly?
+sm = t[:, 5]
+by_sm = {}
+for i in range(len(t)):
+    by_sm.setdefault(int(sm[i]), []).append(i)
+sm_rate = []
+pair_ratio = []
+for k, idx in by_sm.items():
+    r = per_cta[idx]
+    sm_rate.append(r.sum())
+    if len(idx) == 2:
+        pair_ratio.append(max(r) / min(r))
+sm_rate = np.array(sm_rate)
+res["sms"] = len(by_sm)
+res["ctas_per_sm"] = sorted({len(v) for v in by_sm.values()})
+res["per_sm_GBps"] = [float(sm_rate.min()), float(np.median(sm_rate)), float(sm_rate.max())]
+res["intra_sm_rate_ratio"] = [float(min(pair_ratio)), float(np.median(pair_ratio)), float(max(pair_ratio))] if pair_ratio else None
+if "--dump" in sys.argv:
+    res["per_cta"] = [[int(sm[i]), float(per_cta[i]), float(first[i]), float(last[i]), float(exit_[i])]
+                      for i in range(len(t))]
 print(json.dumps(res, indent=1))
