@@ -25,6 +25,7 @@
 // pushes, which come after this rank finished reading epoch e (stream order).
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -393,6 +394,7 @@ int choose_splits(int tiles, int chunks, int npad) {
   const size_t ring = static_cast<size_t>(ring_stages(npad)) *
                       (kTileM * kChunkK * 2 + npad * kChunkK * 2);
   int s = num_sms() / tiles;
+  if (const char* f = std::getenv("OFB_K6_SPLITS")) s = std::atoi(f);   // tuning experiments
   s = std::max(1, std::min(s, std::min(8, chunks)));
   while (s > 1 && static_cast<size_t>(s - 1) * npad * kTileM * 4 + static_cast<size_t>(npad) * kTileM * 2 > ring)
     --s;
