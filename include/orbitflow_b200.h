@@ -132,6 +132,14 @@ typedef struct ofb_step_desc {
   const int64_t* fetch_bytes;  /* [B] bytes fetched per offloaded (b, l) slab */
   int32_t staging_slots;       /* 1 = reference single-slot launch rule, 2 = double buffer */
   int32_t record_timing;       /* 1 = record per-layer / per-copy CUDA events */
+  /* Cross-step prefetch (NULL = off): [B] bytes each request will fetch per
+   * offloaded slab in the NEXT step.  After this step the runtime already
+   * enqueues, per request, the next step's first staging_slots fetches (same
+   * slabs, same slots), each gated on this step's last attention that used
+   * its slot, so the copy engines stay busy while the host turns the step
+   * around.  The next step adopts them if its transfer plan matches, else
+   * they are fenced and re-issued. */
+  const int64_t* next_fetch_bytes;
 } ofb_step_desc;
 
 typedef struct ofb_step_timing {
@@ -176,6 +184,12 @@ OFB_API int ofb_runtime_decode_step(ofb_runtime* rt, const ofb_step_desc* desc, 
 OFB_API int ofb_runtime_step_begin(ofb_runtime* rt, const ofb_step_desc* desc, void* stream);
 OFB_API int ofb_runtime_step_layers(ofb_runtime* rt, int32_t count);
 OFB_API int ofb_runtime_step_end(ofb_runtime* rt);
+/* Make `stream` wait for every cross-step prefetch still in flight and drop
+ * it (call before reusing staging or host slabs, e.g. after a plan change or a
+ * released request). */
+OFB_API int ofb_runtime_prefetch_fence(ofb_runtime* rt, void* stream);
+/* Steps that adopted the previous step's prefetch / prefetches dropped on a plan mismatch. */
+OFB_API int ofb_runtime_prefetch_stats(ofb_runtime* rt, int64_t* adopted, int64_t* dropped);
 
 /* K4: plan-change reconfiguration.  Enqueue n whole-slab moves
  * (kind 0 = host->device restore, 1 = device->host eviction, 2 = device->device)

@@ -39,6 +39,7 @@ class StepDesc(ctypes.Structure):
         ("max_seq_len", c_i32),
         ("host_slabs", c_vp), ("staging_dst", c_vp), ("fetch_bytes", c_vp),
         ("staging_slots", c_i32), ("record_timing", c_i32),
+        ("next_fetch_bytes", c_vp),
     ]
 
 
@@ -112,6 +113,8 @@ SIGNATURES = {
     "ofb_runtime_step_begin": (ctypes.c_int, [c_vp, ctypes.POINTER(StepDesc), c_vp]),
     "ofb_runtime_step_layers": (ctypes.c_int, [c_vp, c_i32]),
     "ofb_runtime_step_end": (ctypes.c_int, [c_vp]),
+    "ofb_runtime_prefetch_fence": (ctypes.c_int, [c_vp, c_vp]),
+    "ofb_runtime_prefetch_stats": (ctypes.c_int, [c_vp, c_i64p, c_i64p]),
     "ofb_runtime_migrate": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "ofb_runtime_timing": (ctypes.c_int, [c_vp, ctypes.POINTER(StepTiming)]),
     "ofb_runtime_migration_pending": (ctypes.c_int, [c_vp, c_i32]),

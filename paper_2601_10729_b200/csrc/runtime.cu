@@ -168,6 +168,20 @@ struct StepValues {
 
 constexpr int kTimingRing = 4;
 
+// Next step's first fetches per request, enqueued at the end of a step.
+struct PrefetchEntry {
+  int b, layer, stream;
+  uint64_t dst, src;
+  int64_t bytes;
+  cudaEvent_t done;
+};
+
+struct PrefetchRec {
+  bool valid = false;
+  std::vector<PrefetchEntry> entries;
+  std::vector<cudaEvent_t> pool;   // timing-disabled, owned here
+};
+
 struct StepState {
   bool active = false;
   ofb_step_desc d{};
@@ -177,6 +191,7 @@ struct StepState {
   std::vector<std::vector<int>> offl;
   std::vector<size_t> next;
   std::vector<cudaEvent_t> attn_done, fetch_done;
+  std::vector<char> adopted;        // [L*B]: fetch already issued by the previous step's prefetch
   std::vector<char> waited_d2h;
   int nstreams = 0;
   bool any_fetch = false;
@@ -205,6 +220,8 @@ struct ofb_runtime {
   // host ranges still being written by the last eviction batch (D2H); fetches
   // reading them wait for mig_done_d2h, everything else overlaps it
   std::vector<std::pair<uint64_t, uint64_t>> pending_d2h;
+  PrefetchRec pf;
+  int64_t pf_adopted = 0, pf_dropped = 0;
 };
 
 namespace {
@@ -276,6 +293,16 @@ int harvest_all(ofb_runtime* rt) {
     int rc = harvest(rt, &rt->ring[(rt->ring_pos + i) % kTimingRing]);
     if (rc) return rc;
   }
+  return 0;
+}
+
+// Every stream in `waiters` waits for all in-flight prefetches; the record is dropped.
+int prefetch_fence(ofb_runtime* rt, const std::vector<cudaStream_t>& waiters) {
+  if (!rt->pf.valid) return 0;
+  for (auto& e : rt->pf.entries)
+    for (cudaStream_t w : waiters) OFB_CUDA(cudaStreamWaitEvent(w, e.done, 0));
+  rt->pf.valid = false;
+  rt->pf.entries.clear();
   return 0;
 }
 
@@ -428,6 +455,7 @@ int ofb_runtime_destroy(ofb_runtime* rt) {
   if (rt->mig_h2d) cudaStreamDestroy(rt->mig_h2d);
   if (rt->mig_d2h) cudaStreamDestroy(rt->mig_d2h);
   for (auto e : rt->sync_events) cudaEventDestroy(e);
+  for (auto e : rt->pf.pool) cudaEventDestroy(e);
   for (auto& rec : rt->ring)
     for (auto e : rec.pool) cudaEventDestroy(e);
   for (cudaEvent_t e : {rt->mig_done_h2d, rt->mig_done_d2h, rt->mig_t0, rt->mig_t1, rt->mig_t2})
@@ -488,6 +516,40 @@ int step_begin(ofb_runtime* rt, const ofb_step_desc* d, cudaStream_t cs) {
   rt->streams_used = st.nstreams;
   if (rec) rec->streams = st.nstreams;
 
+  // Adopt the previous step's prefetch if it fetched exactly this step's first
+  // fetches per request (same slab, slot, size, stream); otherwise fence it.
+  st.adopted.assign((size_t)L * B, 0);
+  if (rt->pf.valid) {
+    // a timed step accounts every copy it makes: it never adopts
+    bool ok = st.nstreams > 0 && !d->record_timing;
+    for (auto& e : rt->pf.entries) {
+      if (!ok) break;
+      if (e.b >= B) { ok = false; break; }
+      const auto& ol = st.offl[e.b];
+      size_t k = 0;
+      while (k < ol.size() && ol[k] != e.layer) ++k;
+      const size_t idx = (size_t)e.layer * B + e.b;
+      ok = k < ol.size() && k < (size_t)d->staging_slots && e.stream == e.b % st.nstreams &&
+           e.dst == d->staging_dst[idx] && e.src == d->host_slabs[idx] && e.bytes == d->fetch_bytes[e.b];
+    }
+    if (ok) {
+      size_t expected = 0;
+      for (int b = 0; b < B; ++b) expected += std::min<size_t>(st.offl[b].size(), (size_t)d->staging_slots);
+      ok = expected == rt->pf.entries.size();
+    }
+    if (ok) {
+      for (auto& e : rt->pf.entries) st.adopted[(size_t)e.layer * B + e.b] = 1;
+      rt->pf_adopted += 1;
+      // the record stays valid until step_layers has consumed its events
+    } else {
+      std::vector<cudaStream_t> waiters(rt->copy.begin(), rt->copy.begin() + st.nstreams);
+      waiters.push_back(cs);
+      rc = prefetch_fence(rt, waiters);
+      if (rc) return rc;
+      rt->pf_dropped += 1;
+    }
+  }
+
   // Step start: the append of every resident row.  Copy streams start after
   // it (staging from the previous step released).  Offloaded rows get their
   // token after their fetch lands (step_layers), so a fetch moves exactly the
@@ -542,6 +604,12 @@ int step_layers(ofb_runtime* rt, int count) {
           OFB_CUDA(cudaStreamWaitEvent(s, st.attn_done[prev], 0));
         }
         const size_t idx = (size_t)dst_layer * B + b;
+        if (st.adopted[idx]) {   // already in flight since the previous step
+          for (auto& e : rt->pf.entries)
+            if (e.b == b && e.layer == dst_layer) st.fetch_done[idx] = e.done;
+          ++st.next[b];
+          continue;
+        }
         if (!rt->pending_d2h.empty() && !st.waited_d2h[b % st.nstreams]) {
           const uint64_t lo = d->host_slabs[idx], hi = lo + (uint64_t)d->fetch_bytes[b];
           for (auto& iv : rt->pending_d2h)
@@ -622,6 +690,41 @@ int step_end(ofb_runtime* rt) {
   if (st.next_layer != st.d.num_layers) return fail(-1, "decode step ended before its last layer");
   for (int b = 0; b < st.d.batch; ++b)
     if (st.next[b] != st.offl[b].size()) return fail(-1, "internal: fetch schedule did not drain");
+  // the adopted prefetch (if any) is consumed: its events were waited on above
+  rt->pf.valid = false;
+  rt->pf.entries.clear();
+  const ofb_step_desc* d = &st.d;
+  if (!d->next_fetch_bytes || !st.any_fetch || d->record_timing) return 0;
+  // Cross-step prefetch: the next step's first S fetches of every request, each
+  // gated on the last attention of this step that read its staging slot (which
+  // also orders it after this step's append into that host slab).
+  const int B = d->batch, S = d->staging_slots;
+  size_t n = 0;
+  for (int b = 0; b < B; ++b) n += std::min<size_t>(st.offl[b].size(), (size_t)S);
+  while (rt->pf.pool.size() < n) {
+    cudaEvent_t e;
+    OFB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    rt->pf.pool.push_back(e);
+  }
+  size_t used = 0;
+  for (int b = 0; b < B; ++b) {
+    const auto& ol = st.offl[b];
+    const size_t K = ol.size();
+    cudaStream_t s = rt->copy[b % st.nstreams];
+    for (size_t k = 0; k < K && k < (size_t)S; ++k) {
+      size_t j_last = k;
+      while (j_last + S < K) j_last += S;   // last fetch of this step into slot k % S
+      OFB_CUDA(cudaStreamWaitEvent(s, st.attn_done[ol[j_last]], 0));
+      const size_t idx = (size_t)ol[k] * B + b;
+      PrefetchEntry e{b, ol[k], b % st.nstreams, d->staging_dst[idx], d->host_slabs[idx],
+                      d->next_fetch_bytes[b], rt->pf.pool[used++]};
+      OFB_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(e.dst), reinterpret_cast<const void*>(e.src),
+                               static_cast<size_t>(e.bytes), cudaMemcpyHostToDevice, s));
+      OFB_CUDA(cudaEventRecord(e.done, s));
+      rt->pf.entries.push_back(e);
+    }
+  }
+  rt->pf.valid = !rt->pf.entries.empty();
   return 0;
 }
 
@@ -655,6 +758,21 @@ int ofb_runtime_step_layers(ofb_runtime* rt, int32_t count) {
 int ofb_runtime_step_end(ofb_runtime* rt) {
   if (!rt) return fail(-1, "ofb_runtime_step_end: null runtime");
   return step_end(rt);
+}
+
+int ofb_runtime_prefetch_stats(ofb_runtime* rt, int64_t* adopted, int64_t* dropped) {
+  if (!rt) return fail(-1, "ofb_runtime_prefetch_stats: null runtime");
+  if (adopted) *adopted = rt->pf_adopted;
+  if (dropped) *dropped = rt->pf_dropped;
+  return 0;
+}
+
+int ofb_runtime_prefetch_fence(ofb_runtime* rt, void* stream) {
+  if (!rt) return fail(-1, "ofb_runtime_prefetch_fence: null runtime");
+  if (rt->step.active) return fail(-1, "ofb_runtime_prefetch_fence: a decode step is in progress");
+  std::vector<cudaStream_t> waiters(rt->copy.begin(), rt->copy.end());
+  waiters.push_back(static_cast<cudaStream_t>(stream));
+  return prefetch_fence(rt, waiters);
 }
 
 int ofb_runtime_migrate(ofb_runtime* rt, int32_t n, const uint64_t* dst, const uint64_t* src,

@@ -81,7 +81,7 @@ class B200Executor:
     def __init__(self, shape: ModelShape, *, device_blocks: int, host_blocks: int,
                  staging_slots: int = 1, copy_streams: int = 16, seed: int = 0,
                  device: str | torch.device = "cuda", record_timing: bool = False,
-                 fill: str = "random"):
+                 fill: str = "random", prefetch_next: bool = True):
         if not torch.cuda.is_available():
             raise RuntimeError("B200Executor needs a CUDA device (there is no CPU fallback)")
         if staging_slots not in (1, 2):
@@ -96,6 +96,9 @@ class B200Executor:
         self.seed = seed
         self.fill = fill
         self.record_timing = record_timing
+        # cross-step prefetch: each step also enqueues the next step's first
+        # fetches (same plan, one more token), adopted if the plan is unchanged
+        self.prefetch_next = prefetch_next
         self.slabs: dict[int, _RequestSlabs] = {}
         self.layout_version = 0
         self._cached_layout = None
@@ -189,6 +192,8 @@ class B200Executor:
 
     def sync_table(self, table, batch, paused=()) -> None:
         """Migrate slabs so physical residency equals ``table.locations``."""
+        # no staging slot or host slab may be reused under an in-flight prefetch
+        self.runtime.prefetch_fence()
         reqs = {r.id: r for r in [*batch, *paused]}
         for rid in [r for r in self.slabs if r not in table.locations]:
             self.release(rid)
@@ -254,6 +259,7 @@ class B200Executor:
         st = self.slabs.pop(rid, None)
         if st is None:
             return
+        self.runtime.prefetch_fence()
         for start in st.dev:
             if start is not None:
                 self.pool.alloc.release(start, st.capacity)
@@ -365,7 +371,12 @@ class B200Executor:
         d.fetch_bytes = fetch.ctypes.data
         d.staging_slots = self.staging_slots
         d.record_timing = int(self.record_timing)
-        keep = (inputs, out, pos_dev, lens_dev, ws, layout, fetch)
+        next_fetch = None
+        if self.prefetch_next and not self.record_timing:
+            next_fetch = np.array([blocks_for_tokens(int(p) + 1, BLOCK_TOKENS) * self.shape.block_bytes
+                                   for p in positions], dtype=np.int64)
+            d.next_fetch_bytes = next_fetch.ctypes.data
+        keep = (inputs, out, pos_dev, lens_dev, ws, layout, fetch, next_fetch)
         return d, keep
 
     def decode_step(self, batch: list[RequestState], placement: PlacementMatrix | None = None,

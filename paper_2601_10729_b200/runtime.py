@@ -44,6 +44,17 @@ class StepRuntime:
     def step_end(self) -> None:
         _native.check(self.lib.ofb_runtime_step_end(self.handle), "ofb_runtime_step_end")
 
+    def prefetch_fence(self, stream=None) -> None:
+        s = stream if stream is not None else torch.cuda.current_stream()
+        _native.check(self.lib.ofb_runtime_prefetch_fence(self.handle, s.cuda_stream),
+                      "ofb_runtime_prefetch_fence")
+
+    def prefetch_stats(self) -> dict:
+        a, d = ctypes.c_int64(), ctypes.c_int64()
+        _native.check(self.lib.ofb_runtime_prefetch_stats(self.handle, ctypes.byref(a), ctypes.byref(d)),
+                      "ofb_runtime_prefetch_stats")
+        return {"adopted": a.value, "dropped": d.value}
+
     def migrate(self, dst: np.ndarray, src: np.ndarray, nbytes: np.ndarray, kinds: np.ndarray,
                 record_timing: bool = False, stream=None) -> None:
         n = len(dst)

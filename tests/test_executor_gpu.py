@@ -344,3 +344,42 @@ def test_reactive_preemption_releases_and_reprefills():
     assert strip == ref
     assert not ex.slabs            # everything released at the end
     ex.close()
+
+
+def test_cross_step_prefetch_is_invisible():
+    """Each step enqueues the next step's first fetches (cross-step prefetch); the
+    next step adopts them when its plan is unchanged and fences them otherwise.
+    Outputs must be bit-identical to running without it, across a plan change
+    (migration + fence) and a released request."""
+    from paper_2601_10729_b200.executor import ModelShape
+
+    shape = ModelShape(6, 8, 2)
+    runs = {}
+    for prefetch in (False, True):
+        batch = [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=300 + 57 * i,
+                              target_output_tokens=40) for i in range(3)]
+        ex = _executor(shape, device_blocks=4000, host_blocks=4000, staging_slots=2, seed=11,
+                       prefetch_next=prefetch)
+        pm = PlacementMatrix.from_strides([0, 1, 2], 6, [2, 1, None])
+        ex.install(batch, pm)
+        outs = []
+        for step in range(9):
+            if step == 4:      # plan change: restores + evictions, prefetch fenced
+                pm = PlacementMatrix.from_strides([0, 1, 2], 6, [1, 2, 3])
+                ex.install(batch, pm)
+            if step == 7:      # request 2 leaves the batch
+                ex.release(2)
+                batch = batch[:2]
+                pm = PlacementMatrix((0, 1), 6, pm.rows[:2])
+            ex.decode_step(batch, pm, ex.synthetic_inputs(len(batch), step=step))
+            outs.append(ex.last_output.clone())
+            if step in (3, 8):
+                _check_step_outputs(ex, batch)
+            for r in batch:
+                r.record_generated_token()
+        runs[prefetch] = (outs, ex.runtime.prefetch_stats())
+        ex.close()
+    for a, b in zip(runs[False][0], runs[True][0]):
+        assert torch.equal(a, b)
+    assert runs[False][1]["adopted"] == 0
+    assert runs[True][1]["adopted"] >= 5, runs[True][1]
