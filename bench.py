@@ -289,8 +289,8 @@ def run_reference_arm(args, cfg):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64-accum over bf16 KV", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "sample": "1 layer (all requests) per step, "
-                                                         "scaled x layers"},
+        "config": {"workload": cfg["workload"],
+                   "sample": f"{samples[0]} layer(s) (all requests) per step, scaled x {cfg['layers']} layers"},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
                          "sample": f"{samples[0]} layer(s) of {cfg['batch']} requests x "
                                    f"{cfg['prompt']} tokens per step, scaled to "
