@@ -394,12 +394,29 @@ def run_ours(args, cfg):
             dist.barrier()
         torch.cuda.synchronize()
 
+    def clean_boundary():
+        """No cross-step prefetch crosses a timing boundary: nothing is in flight
+        when a timed region starts (the first step fetches everything itself) and
+        the last step of a region issues none, so a region holds exactly its own
+        steps' transfers."""
+        ex.drain()
+        ex.runtime.prefetch_fence()
+        barrier()
+
+    def run_steps(n, e2e=False, marks=None):
+        for i in range(n):
+            ex.prefetch_next = i < n - 1
+            step(i, e2e=e2e)
+            if marks is not None:
+                marks.append(time.perf_counter())
+        ex.prefetch_next = True
+
     for i in range(args.warmup):
         step(i)
-    ex.drain()
-    barrier()
-    # The timed steps carry no per-layer / per-copy events: an event between two
-    # kernels breaks their programmatic-dependent-launch overlap.  Per-launch K1
+    clean_boundary()
+    # --layer-events inline (default): per-launch K1 / per-copy events inside the
+    # timed steps.  separate: the timed steps carry none (an event between two
+    # kernels breaks their programmatic-dependent-launch overlap) and per-launch K1
     # times and per-copy bytes come from a separate instrumented pass below.
     inline = args.layer_events == "inline"
     ex.record_timing = inline
@@ -409,23 +426,22 @@ def run_ours(args, cfg):
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record()
-        for i in range(args.steps):
-            step(i)
+        run_steps(args.steps)
         t_end.record()
         ex.drain()
         barrier()
     total_ms = t_start.elapsed_time(t_end)
     if not inline:
+        clean_boundary()
         ex.record_timing = True
         ex.runtime.timing_reset()
         attn_tokens.clear()
-        for i in range(min(args.steps, 3)):
-            step(i)
+        run_steps(min(args.steps, 3))
         ex.drain()
         barrier()
     tm = ex.runtime.timing()   # per-launch K1 events + fetch bytes of the instrumented steps
     k1_tokens = list(attn_tokens)
-    ex.record_timing = inline
+    ex.record_timing = False   # e2e: a serving loop, no instrumentation
     if dist is not None:
         t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -434,12 +450,15 @@ def run_ours(args, cfg):
 
     # e2e through the public API with host buffers (one untimed warm-up step)
     step(0, e2e=True)
-    barrier()
+    clean_boundary()
+    pf0 = ex.runtime.prefetch_stats()
     e0 = time.perf_counter()
     e2e_steps = max(8, args.steps)
-    for i in range(e2e_steps):
-        step(i, e2e=True)
+    marks = [e0]
+    run_steps(e2e_steps, e2e=True, marks=marks)
     barrier()
+    e2e_step_ms = [(b - a) * 1e3 for a, b in zip(marks, marks[1:])]
+    pf1 = ex.runtime.prefetch_stats()
     e2e_ms = (time.perf_counter() - e0) * 1e3 / e2e_steps
     if dist is not None:
         t = torch.tensor([e2e_ms], device=dev)
@@ -508,7 +527,10 @@ def run_ours(args, cfg):
                                  f"{len(k1_tokens)} steps (timed steps carry no per-layer events)"),
                    "l2": "inputs (64 GiB KV) larger than the 126 MB L2; no flush needed"},
         "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
-                "h2d_bytes_per_step": h2d_in, "d2h_bytes_per_step": d2h_out},
+                "h2d_bytes_per_step": h2d_in, "d2h_bytes_per_step": d2h_out,
+                "step_ms": [round(x, 3) for x in e2e_step_ms],
+                "prefetch_adopted_steps": pf1["adopted"] - pf0["adopted"],
+                "prefetch_dropped_steps": pf1["dropped"] - pf0["dropped"]},
         "roofline": {"bound": "hbm", "kernel": "paged_gqa_decode_kernel (K1)",
                      "achieved": attn_gbs, "peak": hbm_peak, "unit": "GB/s",
                      "frac": attn_gbs / hbm_peak,

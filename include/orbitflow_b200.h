@@ -137,8 +137,8 @@ typedef struct ofb_step_desc {
    * enqueues, per request, the next step's first staging_slots fetches (same
    * slabs, same slots), each gated on this step's last attention that used
    * its slot, so the copy engines stay busy while the host turns the step
-   * around.  The next step adopts them if its transfer plan matches, else
-   * they are fenced and re-issued. */
+   * around.  The next step adopts them if its transfer plan matches (and
+   * counts them in its timing record), else they are fenced and re-issued. */
   const int64_t* next_fetch_bytes;
 } ofb_step_desc;
 

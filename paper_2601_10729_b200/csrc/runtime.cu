@@ -173,13 +173,17 @@ struct PrefetchEntry {
   int b, layer, stream;
   uint64_t dst, src;
   int64_t bytes;
-  cudaEvent_t done;
+  cudaEvent_t done, t0, t1;   // t0/t1: timing, handed to the adopting step's record
 };
+
+constexpr int kPrefetchGens = kTimingRing + 1;   // timing events outlive the record that reads them
 
 struct PrefetchRec {
   bool valid = false;
   std::vector<PrefetchEntry> entries;
-  std::vector<cudaEvent_t> pool;   // timing-disabled, owned here
+  std::vector<cudaEvent_t> pool;               // timing-disabled, owned here
+  std::vector<cudaEvent_t> tpool[kPrefetchGens];  // timing-enabled, per generation
+  int gen = 0;
 };
 
 struct StepState {
@@ -273,7 +277,7 @@ int harvest(ofb_runtime* rt, StepRecord* rec) {
     float a = 0, b = 0;
     OFB_CUDA(cudaEventElapsedTime(&a, rec->start, c.start));
     OFB_CUDA(cudaEventElapsedTime(&b, rec->start, c.stop));
-    first = std::min(first, a);
+    first = std::min(first, std::max(a, 0.f));   // adopted prefetches began before the step
     lastc = std::max(lastc, b);
   }
   v.copies = static_cast<int32_t>(rec->copies.size());
@@ -456,6 +460,8 @@ int ofb_runtime_destroy(ofb_runtime* rt) {
   if (rt->mig_d2h) cudaStreamDestroy(rt->mig_d2h);
   for (auto e : rt->sync_events) cudaEventDestroy(e);
   for (auto e : rt->pf.pool) cudaEventDestroy(e);
+  for (auto& v : rt->pf.tpool)
+    for (auto e : v) cudaEventDestroy(e);
   for (auto& rec : rt->ring)
     for (auto e : rec.pool) cudaEventDestroy(e);
   for (cudaEvent_t e : {rt->mig_done_h2d, rt->mig_done_d2h, rt->mig_t0, rt->mig_t1, rt->mig_t2})
@@ -520,8 +526,7 @@ int step_begin(ofb_runtime* rt, const ofb_step_desc* d, cudaStream_t cs) {
   // fetches per request (same slab, slot, size, stream); otherwise fence it.
   st.adopted.assign((size_t)L * B, 0);
   if (rt->pf.valid) {
-    // a timed step accounts every copy it makes: it never adopts
-    bool ok = st.nstreams > 0 && !d->record_timing;
+    bool ok = st.nstreams > 0;
     for (auto& e : rt->pf.entries) {
       if (!ok) break;
       if (e.b >= B) { ok = false; break; }
@@ -538,7 +543,10 @@ int step_begin(ofb_runtime* rt, const ofb_step_desc* d, cudaStream_t cs) {
       ok = expected == rt->pf.entries.size();
     }
     if (ok) {
-      for (auto& e : rt->pf.entries) st.adopted[(size_t)e.layer * B + e.b] = 1;
+      for (auto& e : rt->pf.entries) {
+        st.adopted[(size_t)e.layer * B + e.b] = 1;
+        if (rec) rec->copies.push_back({e.t0, e.t1, static_cast<double>(e.bytes), e.stream});
+      }
       rt->pf_adopted += 1;
       // the record stays valid until step_layers has consumed its events
     } else {
@@ -694,7 +702,7 @@ int step_end(ofb_runtime* rt) {
   rt->pf.valid = false;
   rt->pf.entries.clear();
   const ofb_step_desc* d = &st.d;
-  if (!d->next_fetch_bytes || !st.any_fetch || d->record_timing) return 0;
+  if (!d->next_fetch_bytes || !st.any_fetch) return 0;
   // Cross-step prefetch: the next step's first S fetches of every request, each
   // gated on the last attention of this step that read its staging slot (which
   // also orders it after this step's append into that host slab).
@@ -705,6 +713,13 @@ int step_end(ofb_runtime* rt) {
     cudaEvent_t e;
     OFB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     rt->pf.pool.push_back(e);
+  }
+  auto& tp = rt->pf.tpool[rt->pf.gen];
+  rt->pf.gen = (rt->pf.gen + 1) % kPrefetchGens;
+  while (tp.size() < 2 * n) {
+    cudaEvent_t e;
+    OFB_CUDA(cudaEventCreate(&e));
+    tp.push_back(e);
   }
   size_t used = 0;
   for (int b = 0; b < B; ++b) {
@@ -717,9 +732,12 @@ int step_end(ofb_runtime* rt) {
       OFB_CUDA(cudaStreamWaitEvent(s, st.attn_done[ol[j_last]], 0));
       const size_t idx = (size_t)ol[k] * B + b;
       PrefetchEntry e{b, ol[k], b % st.nstreams, d->staging_dst[idx], d->host_slabs[idx],
-                      d->next_fetch_bytes[b], rt->pf.pool[used++]};
+                      d->next_fetch_bytes[b], rt->pf.pool[used], tp[2 * used], tp[2 * used + 1]};
+      ++used;
+      OFB_CUDA(cudaEventRecord(e.t0, s));
       OFB_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(e.dst), reinterpret_cast<const void*>(e.src),
                                static_cast<size_t>(e.bytes), cudaMemcpyHostToDevice, s));
+      OFB_CUDA(cudaEventRecord(e.t1, s));
       OFB_CUDA(cudaEventRecord(e.done, s));
       rt->pf.entries.push_back(e);
     }

@@ -372,7 +372,7 @@ class B200Executor:
         d.staging_slots = self.staging_slots
         d.record_timing = int(self.record_timing)
         next_fetch = None
-        if self.prefetch_next and not self.record_timing:
+        if self.prefetch_next:
             next_fetch = np.array([blocks_for_tokens(int(p) + 1, BLOCK_TOKENS) * self.shape.block_bytes
                                    for p in positions], dtype=np.int64)
             d.next_fetch_bytes = next_fetch.ctypes.data
