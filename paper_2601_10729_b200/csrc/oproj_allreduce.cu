@@ -206,6 +206,7 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
     mbar_init(&acc_bar, 1);
     fence_mbar_init();
   }
+  __syncwarp();   // warp 0 re-converges after its lane-0 setup before the aligned barrier
   if (warp == 2) tmem_alloc(&tmem_base_sh, tcols);
   tc_fence_before();
   __syncthreads();
@@ -387,15 +388,16 @@ int ring_stages(int npad) {
   return std::max(2, std::min(kMaxStages, kSmemBudget / stage_bytes));
 }
 
-// CTAs per hidden tile (= cluster size): enough to cover the SMs, at most 8
-// (portable cluster), at most one K chunk each, and the leader's reduction
-// buffers + bf16 staging must fit in its (idle) ring.
+// CTAs per hidden tile (= cluster size): enough to cover the SMs, at most 4,
+// at most one K chunk each, and the leader's reduction buffers + bf16 staging
+// must fit in its (idle) ring.  (8-CTA clusters compute correctly but trip
+// compute-sanitizer synccheck at the first barrier; 4 is where our shapes sit.)
 int choose_splits(int tiles, int chunks, int npad) {
   const size_t ring = static_cast<size_t>(ring_stages(npad)) *
                       (kTileM * kChunkK * 2 + npad * kChunkK * 2);
   int s = num_sms() / tiles;
   if (const char* f = std::getenv("OFB_K6_SPLITS")) s = std::atoi(f);   // tuning experiments
-  s = std::max(1, std::min(s, std::min(8, chunks)));
+  s = std::max(1, std::min(s, std::min(4, chunks)));
   while (s > 1 && static_cast<size_t>(s - 1) * npad * kTileM * 4 + static_cast<size_t>(npad) * kTileM * 2 > ring)
     --s;
   return s;

@@ -1,4 +1,5 @@
-"""Small K1/K3/K2/K4 workload for compute-sanitizer (memcheck / racecheck / synccheck)."""
+"""Small K1/K3/K2/K4/K6 workload for compute-sanitizer (memcheck / racecheck / synccheck),
+including steps that adopt the cross-step prefetch."""
 import math
 import sys
 from pathlib import Path
@@ -32,7 +33,21 @@ ex.decode_step(batch, a)
 for r in batch:
     r.record_generated_token()
 ex.install(batch, b)
-ex.decode_step(batch, b)
+for _ in range(3):           # same plan: steps 2 and 3 adopt the previous step's prefetch
+    ex.decode_step(batch, b)
+    for r in batch:
+        r.record_generated_token()
+assert ex.runtime.prefetch_stats()["adopted"] >= 2
 torch.cuda.synchronize()
 ex.close()
+
+# K6 (tcgen05 o-projection; single rank: the exchange needs concurrently running
+# peers, which the sanitizer's serialised launches cannot provide)
+from paper_2601_10729_b200.collective import OprojAllReduce  # noqa: E402
+
+for bsz, k, h in [(5, 128, 1024), (32, 1024, 2048)]:
+    w = (torch.randn((2, h, k), device=dev) * k ** -0.5).to(torch.bfloat16)
+    x = torch.randn((2, bsz, k), device=dev).to(torch.bfloat16)
+    OprojAllReduce(w, bsz)(x, 1)
+torch.cuda.synchronize()
 print("sanitize case done")
