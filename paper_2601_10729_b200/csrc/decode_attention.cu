@@ -407,7 +407,8 @@ cudaError_t launch_decode_attention_stream(const CUtensorMap& map, const void* q
                                            const int32_t* block_tables, int max_blocks,
                                            const int32_t* seq_lens, void* workspace,
                                            size_t workspace_bytes, int batch, int hq, int hkv,
-                                           int max_seq_len, float scale, cudaStream_t stream);
+                                           int max_seq_len, float scale, cudaStream_t stream,
+                                           bool kv_ready);
 
 // K1 work decomposition: "stream" (persistent stream-K, default) or "split"
 // (fixed splits + last-CTA combine); OFB_K1=split selects the latter.
@@ -467,12 +468,13 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
                                     const int32_t* block_tables, int max_blocks,
                                     const int32_t* seq_lens, void* workspace,
                                     size_t workspace_bytes, int batch, int hq, int hkv,
-                                    int max_seq_len, float scale, cudaStream_t stream) {
+                                    int max_seq_len, float scale, cudaStream_t stream,
+                                    bool kv_ready) {
   if (batch <= 0) return cudaSuccess;
   if (!use_split_kernel(batch, hkv, max_seq_len))
     return launch_decode_attention_stream(map, q, out, block_tables, max_blocks, seq_lens,
                                           workspace, workspace_bytes, batch, hq, hkv, max_seq_len,
-                                          scale, stream);
+                                          scale, stream, kv_ready);
   if (hkv <= 0 || hq % hkv != 0 || hq / hkv > kMaxGroup) return cudaErrorInvalidValue;
   if ((size_t)batch * hkv * sizeof(int32_t) > kCounterRegionBytes) return cudaErrorInvalidValue;
   cudaError_t e = attn_init_once();

@@ -42,6 +42,7 @@ struct StreamArgs {
   int32_t* counters;  // [B * Hkv], zero at rest
   int max_blocks, batch, hq, hkv, group, grid;
   float scale_log2;
+  int kv_ready;       // 1: KV is complete before the PDL wait - the producer may stream early
   unsigned long long* trace;  // diagnostics (ofb_k1_trace): per CTA globaltimer stamps, or null
 };
 
@@ -138,7 +139,10 @@ paged_gqa_decode_stream_kernel(const __grid_constant__ CUtensorMap kv_map, const
   // Everything above touched only launch inputs; the previous kernel on the
   // stream (an append into this layer's slabs, an o-projection producing q,
   // the previous layer's K1 sharing this workspace) must be complete past here.
-  pdl_wait();
+  // With kv_ready the host guarantees this layer's KV was complete before the
+  // previous kernel started, so the producer streams it while that kernel
+  // drains (only the ring fills: consumers still wait for q).
+  if (!(a.kv_ready && warp == kSConsumers)) pdl_wait();
   pdl_trigger();
   if (tr) tr[1] = gtimer();
 
@@ -249,9 +253,9 @@ paged_gqa_decode_stream_kernel(const __grid_constant__ CUtensorMap kv_map, const
     if (!whole) {
       // last of the pair's CTAs to arrive combines its partials
       const int c_lo = sp.cta_of(pb), c_hi = sp.cta_of(pe - 1);
-      __threadfence();
-      consumer_bar();
-      if (tid == 0) {
+      consumer_bar();        // every partial write of the CTA happens-before thread 0's
+      if (tid == 0) {        // gpu-scope fence + ticket (cumulative release)
+        __threadfence();
         const int ticket = atomicAdd(&a.counters[p], 1);
         *flag = (ticket == c_hi - c_lo);
       }
@@ -379,7 +383,8 @@ cudaError_t launch_decode_attention_stream(const CUtensorMap& map, const void* q
                                            const int32_t* block_tables, int max_blocks,
                                            const int32_t* seq_lens, void* workspace,
                                            size_t workspace_bytes, int batch, int hq, int hkv,
-                                           int max_seq_len, float scale, cudaStream_t stream) {
+                                           int max_seq_len, float scale, cudaStream_t stream,
+                                           bool kv_ready) {
   if (batch <= 0) return cudaSuccess;
   if (batch > kSMaxBatch || hkv <= 0 || hq % hkv != 0 || hq / hkv > kMaxGroup)
     return cudaErrorInvalidValue;
@@ -399,6 +404,7 @@ cudaError_t launch_decode_attention_stream(const CUtensorMap& map, const void* q
   a.ws_o = reinterpret_cast<float*>(ws + kSCounterBytes +
                                     (size_t)kSMaxGrid * 2 * kMaxGroup * sizeof(float));
   a.trace = k1_trace_buffer();
+  a.kv_ready = kv_ready ? 1 : 0;
   a.max_blocks = max_blocks;
   a.batch = batch;
   a.hq = hq;

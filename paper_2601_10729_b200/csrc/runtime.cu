@@ -24,7 +24,8 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
                                     const int32_t* block_tables, int max_blocks,
                                     const int32_t* seq_lens, void* workspace,
                                     size_t workspace_bytes, int batch, int hq, int hkv,
-                                    int max_seq_len, float scale, cudaStream_t stream);
+                                    int max_seq_len, float scale, cudaStream_t stream,
+                                    bool kv_ready = false);
 cudaError_t launch_kv_append(const void* k_new, const void* v_new, void* pool,
                              const int32_t* block_tables, int max_blocks,
                              const int32_t* positions, const uint64_t* host_slabs,
@@ -670,11 +671,15 @@ int step_layers(ofb_runtime* rt, int count) {
       if ((rc = next_timing_event(rec, &t0)) || (rc = next_timing_event(rec, &t1))) return rc;
       OFB_CUDA(cudaEventRecord(t0, cs));
     }
+    // KV of a layer with no fetch this step was complete before the previous
+    // layer's K1 passed its dependency wait (step-start append), so K1 may stream
+    // it before its own wait; q / outputs / workspace still wait.
+    const bool kv_ready = l > 0 && !layer_fetches;
     e = ofb::launch_decode_attention(
         st.map, static_cast<const uint8_t*>(d->q) + l * q_layer,
         static_cast<uint8_t*>(d->out) + l * q_layer, d->block_tables + l * bt_layer, d->max_blocks,
         d->seq_lens, d->workspace, static_cast<size_t>(d->workspace_bytes), B, d->num_q_heads,
-        d->num_kv_heads, d->max_seq_len, d->scale, cs);
+        d->num_kv_heads, d->max_seq_len, d->scale, cs, kv_ready);
     if (e != cudaSuccess) return cuda_fail(e, "paged_gqa_decode_kernel launch");
     if (rec) {
       OFB_CUDA(cudaEventRecord(t1, cs));
