@@ -11,9 +11,11 @@
  *     (/root/reference/pkg/src/kvsim) contains no attention arithmetic - it
  *     prices it as per_layer_compute (core.py:257-261) - and the paper's
  *     implementation lives in un-vendored vLLM v0.6.6 PagedAttention.  This
- *     attention oracle is therefore pinned only against an independent
- *     float64 dense softmax(QK^T)V (tests/test_oracle.py), not against
- *     reference outputs: "parity unpinned by the reference".
+ *     attention oracle is therefore pinned against an independent float64
+ *     dense softmax(QK^T)V and against golden outputs of vLLM's
+ *     PagedAttention v2 kernel (0.22, same kernel family) recorded on a B200
+ *     (tests/golden/vllm_attention.npz, tests/test_oracle.py) - not against
+ *     kvsim outputs, which do not exist: "parity unpinned by the reference".
  *   - the new-token append (RequestState.record_generated_token,
  *     core.py:95-102; engine.py:389-392): the row lands at token index
  *     `pos` of the slab, i.e. block pos/16, slot pos%16.
