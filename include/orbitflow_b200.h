@@ -253,9 +253,16 @@ typedef struct ofb_oproj_desc {
   uint32_t epoch;      /* > 0, +1 per call, identical on every rank */
   int32_t* status;     /* device int32: set to 1 if a peer's tile never arrived (timeout) */
   int64_t timeout_ns;  /* spin limit per tile wait (0 = 5 s) */
+  int32_t w_layout;    /* 0: w is [layers][hidden][k] (Linear); 1: packed
+                          [layers][hidden/128][k/64][128][64] - every TMA box a
+                          contiguous 16 KiB (weights are static: pack once) */
 } ofb_oproj_desc;
 
 OFB_API int ofb_oproj_allreduce(const ofb_oproj_desc* desc, void* stream);
+/* Diagnostics: K6 launches write globaltimer stamps per CTA (entry, prologue done,
+ * accumulator ready, cluster synced, output start, exit) into `device_buffer`
+ * (uint64 [grid][8]); NULL switches tracing off. */
+OFB_API int ofb_k6_trace(void* device_buffer);
 
 /* ---- native exact placement solver (host code, no GPU needed) ---------- */
 /* Bit-exact restatement of kvsim solve / solve_capacity_only

@@ -89,6 +89,7 @@ class OprojDesc(ctypes.Structure):
         ("workspace", c_vp), ("workspace_bytes", c_i64),
         ("world", c_i32), ("rank", c_i32), ("max_batch", c_i32),
         ("symm", c_vp * 8), ("epoch", ctypes.c_uint32), ("status", c_vp), ("timeout_ns", c_i64),
+        ("w_layout", c_i32),
     ]
 
 
@@ -127,6 +128,7 @@ SIGNATURES = {
     "ofb_oproj_symm_bytes": (c_i64, [c_i32, c_i32, c_i32]),
     "ofb_oproj_workspace_bytes": (c_i64, [c_i32, c_i32, c_i32]),
     "ofb_oproj_allreduce": (ctypes.c_int, [ctypes.POINTER(OprojDesc), c_vp]),
+    "ofb_k6_trace": (ctypes.c_int, [c_vp]),
     "ofb_plan_solve": (ctypes.c_int, [ctypes.POINTER(PlanProblem), ctypes.POINTER(PlanResult)]),
     "ofb_plan_last_error": (ctypes.c_char_p, []),
     "ofb_link_probe": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, ctypes.POINTER(c_f64),

@@ -144,13 +144,20 @@ class OprojAllReduce:
     """
 
     def __init__(self, w_o: torch.Tensor, max_batch: int, symm: SymmetricBuffers | None = None,
-                 timeout_ns: int = 0):
+                 timeout_ns: int = 0, pack: bool = True):
         if not w_o.is_cuda or w_o.dtype != torch.bfloat16 or w_o.dim() != 3:
             raise ValueError("w_o must be a bf16 CUDA tensor [layers, hidden, k]")
-        self.w = w_o.contiguous()
-        self.layers, self.hidden, self.k = self.w.shape
+        self.layers, self.hidden, self.k = w_o.shape
         if self.k % 64 or self.hidden % 128:
             raise ValueError("k must be a multiple of 64 and hidden of 128")
+        # Weights are static: pack once so that every TMA box the kernel loads
+        # (128 rows x 64 k of one hidden tile) is 16 KiB contiguous in HBM.
+        self.w_layout = 1 if pack else 0
+        if pack:
+            self.w = (w_o.reshape(self.layers, self.hidden // 128, 128, self.k // 64, 64)
+                      .permute(0, 1, 3, 2, 4).contiguous())
+        else:
+            self.w = w_o.contiguous()
         if symm is not None and (symm.hidden != self.hidden or symm.max_batch < max_batch):
             raise ValueError("symmetric buffers sized for another hidden / batch")
         self.max_batch = max_batch
@@ -183,6 +190,7 @@ class OprojAllReduce:
         d.max_batch = self.max_batch
         d.status = self._status.data_ptr()
         d.timeout_ns = self.timeout_ns
+        d.w_layout = self.w_layout
         if self.symm is None or self.symm.world == 1:
             d.world, d.rank, d.epoch = 1, 0, 1
             if self.symm is not None:

@@ -56,7 +56,8 @@ struct OprojArgs {
   __nv_bfloat16* out;       // [batch][hidden]
   int* status;
   char* symm[kMaxPeers];
-  long long flags_off;      // byte offset of the flags inside a symmetric buffer
+  long long flags_off;
+  unsigned long long* trace;   // diagnostics (ofb_k6_trace): per CTA stamps, or null      // byte offset of the flags inside a symmetric buffer
 };
 
 // ---------------------------------------------------------------- tcgen05
@@ -135,6 +136,16 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_4d(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];"
+      ::"r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)),
+        "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
 // ---------------------------------------------------------------- system-scope flags
 __device__ __forceinline__ void st_release_sys(unsigned int* p, unsigned int v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -190,6 +201,8 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x / a.splits, split = blockIdx.x % a.splits;   // split = rank in cluster
+  unsigned long long* tr = (a.trace && threadIdx.x == 0) ? a.trace + (size_t)blockIdx.x * 8 : nullptr;
+  if (tr) tr[0] = globaltimer();
   const int c0 = split * a.chunks / a.splits;
   const int nchunks = (split + 1) * a.chunks / a.splits - c0;
   const int stage_w = kTileM * kChunkK * 2;          // 16 KiB of W rows
@@ -212,6 +225,7 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
+  if (tr) tr[1] = globaltimer();
 
   if (warp == 0 && lane == 0) {
     // TMA producer.  W_o does not depend on the previous kernel (attention), so
@@ -220,7 +234,7 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
     const int pre = nchunks < a.stages ? nchunks : a.stages;
     for (int i = 0; i < pre; ++i) {
       mbar_arrive_expect_tx(&full_bar[i], stage_bytes);
-      tma_load_3d(smem + i * stage_bytes, &wmap, &full_bar[i], (c0 + i) * kChunkK, tile * kTileM, a.layer);
+      tma_load_4d(smem + i * stage_bytes, &wmap, &full_bar[i], 0, 0, c0 + i, a.layer * a.tiles + tile);
     }
     pdl_wait();
     for (int i = 0; i < pre; ++i)
@@ -230,7 +244,7 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
       mbar_wait(&empty_bar[s], (round - 1) & 1);
       uint8_t* sw = smem + s * stage_bytes;
       mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
-      tma_load_3d(sw, &wmap, &full_bar[s], (c0 + i) * kChunkK, tile * kTileM, a.layer);
+      tma_load_4d(sw, &wmap, &full_bar[s], 0, 0, c0 + i, a.layer * a.tiles + tile);
       tma_load_3d(sw + stage_w, &xmap, &full_bar[s], (c0 + i) * kChunkK, 0, a.layer);
     }
   } else if (warp == 1 && lane == 0) {
@@ -253,6 +267,7 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
 
   // ---- epilogue (row m = warp*32 + lane of the tile)
   mbar_wait(&acc_bar, 0);
+  if (tr) tr[2] = globaltimer();
   tc_fence_after();
   pdl_wait();                       // every thread: the predecessor's writes are visible
   pdl_trigger();                    // the next kernel may start its own prologue
@@ -264,6 +279,7 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
   __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(smem + static_cast<size_t>(a.splits - 1) * a.npad * kTileM * 4);
   if (a.splits > 1) {
     cluster_sync_all();             // every CTA of the cluster is past its MMAs
+    if (tr) tr[3] = globaltimer();
     if (split != 0) {
       const uint32_t dst = map_to_cta(smem_u32(red + static_cast<size_t>(split - 1) * a.npad * kTileM), 0);
       for (int c = 0; c < a.npad / 32; ++c) {
@@ -276,6 +292,7 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
       __syncthreads();
       if (warp == 2) tmem_dealloc(tmem, tcols);
       cluster_sync_all();           // partials visible in the leader
+      if (tr) tr[5] = globaltimer();
       return;
     }
     cluster_sync_all();
@@ -300,11 +317,13 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
 
   const int nvec = a.batch * (kTileM / 8);     // 16-byte vectors of the [batch][128] tile
   const uint4* s4 = reinterpret_cast<const uint4*>(stg);
+  if (tr) tr[4] = globaltimer();
   if (a.world == 1) {
     for (int i = threadIdx.x; i < nvec; i += kThreads) {
       const int b = i >> 4, o = i & 15;
       *reinterpret_cast<uint4*>(a.out + static_cast<size_t>(b) * a.hidden + tile * kTileM + o * 8) = s4[i];
     }
+    if (tr) tr[5] = globaltimer();
     return;
   }
 
@@ -414,9 +433,10 @@ size_t flags_bytes(int world, int hidden) {
 struct MapKey {
   const void* x;
   const void* w;
-  int layers, batch, k, hidden, npad;
+  int layers, batch, k, hidden, npad, w_layout;
   CUtensorMap xmap, wmap;
 };
+unsigned long long* g_k6_trace = nullptr;
 std::mutex g_map_mu;
 std::vector<MapKey> g_map_cache;
 
@@ -424,12 +444,12 @@ int get_maps(const ofb_oproj_desc* d, int npad, CUtensorMap* xmap, CUtensorMap* 
   std::lock_guard<std::mutex> lock(g_map_mu);
   for (auto& e : g_map_cache)
     if (e.x == d->x && e.w == d->w && e.layers == d->layers && e.batch == d->batch &&
-        e.k == d->k && e.hidden == d->hidden && e.npad == npad) {
+        e.k == d->k && e.hidden == d->hidden && e.npad == npad && e.w_layout == d->w_layout) {
       *xmap = e.xmap;
       *wmap = e.wmap;
       return 0;
     }
-  MapKey e{d->x, d->w, d->layers, d->batch, d->k, d->hidden, npad, {}, {}};
+  MapKey e{d->x, d->w, d->layers, d->batch, d->k, d->hidden, npad, d->w_layout, {}, {}};
   const uint64_t row = static_cast<uint64_t>(d->k) * 2;
   {  // X: [layers][batch][k]; box 64 x npad x 1 (rows past the batch read as zero)
     uint64_t dims[3] = {static_cast<uint64_t>(d->k), static_cast<uint64_t>(d->batch),
@@ -439,12 +459,25 @@ int get_maps(const ofb_oproj_desc* d, int npad, CUtensorMap* xmap, CUtensorMap* 
     int rc = encode_bf16_map(&e.xmap, const_cast<void*>(d->x), 3, dims, strides, box);
     if (rc) return rc;
   }
-  {  // W: [layers][hidden][k]; box 64 x 128 x 1
-    uint64_t dims[3] = {static_cast<uint64_t>(d->k), static_cast<uint64_t>(d->hidden),
-                        static_cast<uint64_t>(d->layers)};
-    uint64_t strides[2] = {row, row * d->hidden};
-    uint32_t box[3] = {static_cast<uint32_t>(kChunkK), static_cast<uint32_t>(kTileM), 1};
-    int rc = encode_bf16_map(&e.wmap, const_cast<void*>(d->w), 3, dims, strides, box);
+  {  // W as 4-D (element in chunk, row in tile, K chunk, layer*tiles + tile); box 64 x 128 x 1 x 1.
+    // Linear layout [layers][hidden][k]: a box is 128 rows x 128 B, rows k*2 B apart.
+    // Packed layout [layers][hidden/128][k/64][128][64]: a box is 16 KiB contiguous.
+    const uint64_t chunks = static_cast<uint64_t>(d->k) / kChunkK;
+    const uint64_t tiles = static_cast<uint64_t>(d->hidden) / kTileM;
+    uint64_t dims[4] = {static_cast<uint64_t>(kChunkK), static_cast<uint64_t>(kTileM), chunks,
+                        tiles * static_cast<uint64_t>(d->layers)};
+    uint64_t strides[3];
+    if (d->w_layout == 1) {
+      strides[0] = kChunkK * 2;                         // row in tile
+      strides[1] = kChunkK * 2 * kTileM;                // next K chunk: 16 KiB
+      strides[2] = strides[1] * chunks;                 // next tile
+    } else {
+      strides[0] = row;                                 // row in tile
+      strides[1] = kChunkK * 2;                         // next K chunk: 128 B along the row
+      strides[2] = row * kTileM;                        // next tile: 128 rows
+    }
+    uint32_t box[4] = {static_cast<uint32_t>(kChunkK), static_cast<uint32_t>(kTileM), 1, 1};
+    int rc = encode_bf16_map(&e.wmap, const_cast<void*>(d->w), 4, dims, strides, box);
     if (rc) return rc;
   }
   if (g_map_cache.size() > 256) g_map_cache.erase(g_map_cache.begin());
@@ -505,6 +538,11 @@ int ofb_ipc_close_handle(void* ptr) {
   return 0;
 }
 
+int ofb_k6_trace(void* device_buffer) {
+  ofb::g_k6_trace = static_cast<unsigned long long*>(device_buffer);
+  return 0;
+}
+
 int64_t ofb_oproj_symm_bytes(int32_t world, int32_t max_batch, int32_t hidden) {
   if (world < 1 || world > ofb::kMaxPeers || max_batch < 1 || hidden < ofb::kTileM) return -1;
   const size_t inbox = (ofb::inbox_bytes(world, max_batch, hidden) + 255) / 256 * 256;
@@ -527,6 +565,7 @@ int ofb_oproj_allreduce(const ofb_oproj_desc* d, void* stream) {
   if (d->hidden < kTileM || d->hidden % kTileM)
     return report_error(-1, "ofb_oproj_allreduce: hidden must be a multiple of 128");
   if (d->layer < 0 || d->layer >= d->layers) return report_error(-1, "ofb_oproj_allreduce: layer out of range");
+  if (d->w_layout != 0 && d->w_layout != 1) return report_error(-1, "ofb_oproj_allreduce: w_layout must be 0 or 1");
   if (d->world < 1 || d->world > kMaxPeers || d->rank < 0 || d->rank >= d->world)
     return report_error(-1, "ofb_oproj_allreduce: bad world / rank");
   if (d->world > 1) {
@@ -562,6 +601,7 @@ int ofb_oproj_allreduce(const ofb_oproj_desc* d, void* stream) {
   a.out = static_cast<__nv_bfloat16*>(d->out);
   a.status = d->status;
   for (int r = 0; r < d->world; ++r) a.symm[r] = static_cast<char*>(d->symm[r]);
+  a.trace = g_k6_trace;
   a.flags_off = static_cast<long long>((inbox_bytes(d->world, d->max_batch, d->hidden) + 255) / 256 * 256);
 
   const size_t smem = static_cast<size_t>(a.stages) * stage_bytes + 1024;

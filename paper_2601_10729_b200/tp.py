@@ -122,10 +122,10 @@ class TensorParallelDecoder:
         lo, hi = shard.q_heads.start * 128, shard.q_heads.stop * 128
         scale = full_k ** -0.5
         # nn.Linear layout [hidden, Hq*128]; this rank multiplies its heads' columns
-        self.w_o = torch.empty((L, hidden, hi - lo), dtype=torch.bfloat16, device=executor.device)
+        w_o = torch.empty((L, hidden, hi - lo), dtype=torch.bfloat16, device=executor.device)
         for l in range(L):
             w = torch.randn((hidden, full_k), generator=g, device=executor.device) * scale
-            self.w_o[l] = w[:, lo:hi].to(torch.bfloat16)
+            w_o[l] = w[:, lo:hi].to(torch.bfloat16)
         world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
         self.symm = None
         if world > 1:
@@ -133,8 +133,18 @@ class TensorParallelDecoder:
                 raise ValueError("process group size differs from the head shard's world")
             self.symm = SymmetricBuffers(world, shard.rank, max_batch, hidden, group=group,
                                          device=executor.device)
-        self.proj = OprojAllReduce(self.w_o, max_batch, self.symm)
+        self.proj = OprojAllReduce(w_o, max_batch, self.symm)   # keeps only the packed copy
+        del w_o
         self.last_hidden = None
+
+    @property
+    def w_o(self) -> torch.Tensor:
+        """This rank's W_o rows [L, hidden, Hq_local*128] (Linear layout), unpacked."""
+        w = self.proj.w
+        if self.proj.w_layout == 0:
+            return w
+        L, tiles, chunks = w.shape[:3]
+        return w.permute(0, 1, 3, 2, 4).reshape(L, tiles * 128, chunks * 64)
 
     def step(self, batch, inputs=None) -> torch.Tensor:
         ex = self.ex
