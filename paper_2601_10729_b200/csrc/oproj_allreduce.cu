@@ -12,7 +12,9 @@
 //
 // Split-K spreads the hidden tiles over every SM: the CTAs of one tile form a
 // thread-block cluster, the non-leaders ship their fp32 partial into the
-// leader's shared memory (DSMEM) and the leader sums in split order.  It then
+// leader's shared memory (DSMEM) - a reduction region of its own, so they need
+// not wait for the leader's MMAs - and one cluster barrier later the leader sums
+// in split order.  It then
 // pushes the bf16 tile into every peer's inbox slot for this rank (P2P stores
 // over NVLink into IPC-mapped symmetric buffers), raises the tile's flag on
 // each peer (st.release.sys), waits for every rank's flag on its own copy of
@@ -225,6 +227,9 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
+  // every CTA of the cluster has started before any DSMEM access (off the critical
+  // path: with PDL this prologue overlaps the previous kernel)
+  if (a.splits > 1) cluster_sync_all();
   if (tr) tr[1] = globaltimer();
 
   if (warp == 0 && lane == 0) {
@@ -273,29 +278,32 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
   pdl_trigger();                    // the next kernel may start its own prologue
   const int m = warp * 32 + lane;
   const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-  // leader smem (the ring is idle once every MMA of the cluster completed):
-  //   red [splits-1][npad][128] fp32 | stg [npad][128] bf16
-  float* red = reinterpret_cast<float*>(smem);
-  __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(smem + static_cast<size_t>(a.splits - 1) * a.npad * kTileM * 4);
-  if (a.splits > 1) {
-    cluster_sync_all();             // every CTA of the cluster is past its MMAs
-    if (tr) tr[3] = globaltimer();
-    if (split != 0) {
-      const uint32_t dst = map_to_cta(smem_u32(red + static_cast<size_t>(split - 1) * a.npad * kTileM), 0);
-      for (int c = 0; c < a.npad / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(trow + c * 32, v);
+  // leader smem: red [splits-1][npad][128] fp32 after the ring (its own region, so
+  // non-leaders may write it while the leader's MMAs still run), stg [npad][128]
+  // bf16 in the ring (idle once the leader's own MMAs completed)
+  float* red = reinterpret_cast<float*>(smem + static_cast<size_t>(a.stages) * stage_bytes);
+  __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(smem);
+  if (a.splits > 1 && split != 0) {
+    // ship this split's fp32 partial into the leader's smem
+    const uint32_t dst = map_to_cta(smem_u32(red + static_cast<size_t>(split - 1) * a.npad * kTileM), 0);
+    for (int c = 0; c < a.npad / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld32(trow + c * 32, v);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) st_cluster_f32(dst + ((c * 32 + j) * kTileM + m) * 4, __uint_as_float(v[j]));
-      }
-      tc_fence_before();
-      __syncthreads();
-      if (warp == 2) tmem_dealloc(tmem, tcols);
-      cluster_sync_all();           // partials visible in the leader
-      if (tr) tr[5] = globaltimer();
-      return;
+      for (int j = 0; j < 32; ++j) st_cluster_f32(dst + ((c * 32 + j) * kTileM + m) * 4, __uint_as_float(v[j]));
     }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) tmem_dealloc(tmem, tcols);
+    // one cluster barrier: the partials are visible in the leader past it, and the
+    // leader (whose smem they target) cannot have exited before it
     cluster_sync_all();
+    if (tr) tr[5] = globaltimer();
+    return;
+  }
+  if (a.splits > 1) {
+    cluster_sync_all();               // every non-leader's partial has landed
+    if (tr) tr[3] = globaltimer();
   }
   for (int c = 0; c < a.npad / 32; ++c) {
     uint32_t v[32];
@@ -402,22 +410,27 @@ int num_sms() {
   return sms;
 }
 
-int ring_stages(int npad) {
+size_t red_bytes(int splits, int npad) {
+  return static_cast<size_t>(splits - 1) * npad * kTileM * 4;
+}
+
+int ring_stages(int npad, int splits) {
   const int stage_bytes = kTileM * kChunkK * 2 + npad * kChunkK * 2;
-  return std::max(2, std::min(kMaxStages, kSmemBudget / stage_bytes));
+  const long avail = static_cast<long>(kSmemBudget) - static_cast<long>(red_bytes(splits, npad));
+  return std::max(2, std::min<int>(kMaxStages, static_cast<int>(avail / stage_bytes)));
 }
 
 // CTAs per hidden tile (= cluster size): enough to cover the SMs, at most 4,
-// at most one K chunk each, and the leader's reduction buffers + bf16 staging
-// must fit in its (idle) ring.  (8-CTA clusters compute correctly but trip
+// at most one K chunk each, and the leader's reduction buffers must fit beside
+// a ring of at least 2 stages.  (8-CTA clusters compute correctly but tripped
 // compute-sanitizer synccheck at the first barrier; 4 is where our shapes sit.)
 int choose_splits(int tiles, int chunks, int npad) {
-  const size_t ring = static_cast<size_t>(ring_stages(npad)) *
-                      (kTileM * kChunkK * 2 + npad * kChunkK * 2);
   int s = num_sms() / tiles;
   if (const char* f = std::getenv("OFB_K6_SPLITS")) s = std::atoi(f);   // tuning experiments
   s = std::max(1, std::min(s, std::min(4, chunks)));
-  while (s > 1 && static_cast<size_t>(s - 1) * npad * kTileM * 4 + static_cast<size_t>(npad) * kTileM * 2 > ring)
+  // the reduction buffers + a 2-stage ring must fit; the bf16 staging reuses the ring
+  const int stage_bytes = kTileM * kChunkK * 2 + npad * kChunkK * 2;
+  while (s > 1 && red_bytes(s, npad) + 2 * static_cast<size_t>(stage_bytes) > static_cast<size_t>(kSmemBudget))
     --s;
   return s;
 }
@@ -592,7 +605,7 @@ int ofb_oproj_allreduce(const ofb_oproj_desc* d, void* stream) {
   a.splits = splits;
   a.chunks = chunks;
   const int stage_bytes = kTileM * kChunkK * 2 + npad * kChunkK * 2;
-  a.stages = ring_stages(npad);
+  a.stages = ring_stages(npad, splits);
   a.world = d->world;
   a.rank = d->rank;
   a.max_batch = d->max_batch;
@@ -604,7 +617,7 @@ int ofb_oproj_allreduce(const ofb_oproj_desc* d, void* stream) {
   a.trace = g_k6_trace;
   a.flags_off = static_cast<long long>((inbox_bytes(d->world, d->max_batch, d->hidden) + 255) / 256 * 256);
 
-  const size_t smem = static_cast<size_t>(a.stages) * stage_bytes + 1024;
+  const size_t smem = static_cast<size_t>(a.stages) * stage_bytes + red_bytes(splits, npad) + 1024;
   static size_t configured = 0;
   if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(oproj_allreduce_kernel,
