@@ -158,6 +158,22 @@ def _standalone_k1(ex, batch, placement, inputs, iters: int = 8):
     return float(np.median(times))
 
 
+def _stream_summary(per_stream, nominal_gbs, peak_gbs):
+    """Host-link GB/s per copy stream: bytes / the stream's busy time (sum of its
+    copies' spans).  The copy engine runs the streams' slab copies essentially one
+    at a time at the full link rate, so each stream's rate while busy is the link
+    rate and the busy times add up to the step's copy span."""
+    rates = [s["bytes"] / (s["busy_ms"] * 1e-3) / 1e9 for s in per_stream if s["busy_ms"] > 0]
+    if not rates:
+        return None
+    return {"streams": len(rates), "GBps_while_busy_min": min(rates),
+            "GBps_while_busy_median": statistics.median(rates), "GBps_while_busy_max": max(rates),
+            "median_over_h2d_peak": statistics.median(rates) / peak_gbs,
+            "median_over_pcie5_nominal": statistics.median(rates) / nominal_gbs,
+            "busy_ms_sum": sum(s["busy_ms"] for s in per_stream),
+            "bytes_per_stream": [s["bytes"] for s in per_stream][:16]}
+
+
 def _mem_available() -> int:
     try:
         for line in open("/proc/meminfo"):
@@ -440,6 +456,7 @@ def run_ours(args, cfg):
         ex.drain()
         barrier()
     tm = ex.runtime.timing()   # per-launch K1 events + fetch bytes of the instrumented steps
+    per_stream = ex.runtime.stream_stats()
     k1_tokens = list(attn_tokens)
     ex.record_timing = False   # e2e: a serving loop, no instrumentation
     if dist is not None:
@@ -556,7 +573,8 @@ def run_ours(args, cfg):
                                                    if copy_span else None),
                           "frac_of_pcie5_nominal": host_alg / (ms_per_step * 1e-3) / 1e9
                           / PCIE5_NOMINAL_GBS,
-                          "blocks_to_fetch_check": blocks_to_fetch(placement, batch)},
+                          "blocks_to_fetch_check": blocks_to_fetch(placement, batch),
+                          "per_copy_stream": _stream_summary(per_stream, PCIE5_NOMINAL_GBS, h2d_peak)},
         "attn_share_of_step": tm["acc_attn_ms"] / max(tm["acc_step_ms"], 1e-9),
         "gpu_launches": args.steps * (1 + L + len({l for row in placement.rows
                                                    for l, b in enumerate(row) if b == 0})

@@ -213,6 +213,10 @@ OFB_API int ofb_runtime_migration_pending(ofb_runtime* rt, int32_t wait);
  * the host can keep enqueuing without waiting). */
 OFB_API int ofb_runtime_timing(ofb_runtime* rt, ofb_step_timing* out);
 OFB_API int ofb_runtime_timing_reset(ofb_runtime* rt);
+/* Per copy stream over the same timed steps: bytes fetched and busy time (sum of
+ * that stream's copy spans); `streams` returns how many streams carried copies. */
+OFB_API int ofb_runtime_stream_stats(ofb_runtime* rt, int32_t max_streams, double* bytes,
+                                     double* busy_ms, int32_t* streams);
 
 /* ---- K6 / C1: o-projection + all-reduce over peer memory (TP) ----------- */
 /* after each layer's attention a KV-head-sharded rank holds

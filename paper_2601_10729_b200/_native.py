@@ -120,6 +120,8 @@ SIGNATURES = {
     "ofb_runtime_timing": (ctypes.c_int, [c_vp, ctypes.POINTER(StepTiming)]),
     "ofb_runtime_migration_pending": (ctypes.c_int, [c_vp, c_i32]),
     "ofb_runtime_timing_reset": (ctypes.c_int, [c_vp]),
+    "ofb_runtime_stream_stats": (ctypes.c_int, [c_vp, c_i32, ctypes.POINTER(c_f64),
+                                                ctypes.POINTER(c_f64), c_i32p]),
     "ofb_symm_alloc": (ctypes.c_int, [c_i64, ctypes.POINTER(c_vp)]),
     "ofb_symm_free": (ctypes.c_int, [c_vp]),
     "ofb_ipc_get_handle": (ctypes.c_int, [c_vp, c_vp]),

@@ -216,6 +216,8 @@ struct ofb_runtime {
   StepValues last;
   int32_t acc_steps = 0, acc_launches = 0;
   double acc_attn_ms = 0, acc_copy_bytes = 0, acc_step_ms = 0;
+  // per copy stream, accumulated like the above: bytes and busy time (sum of copy spans)
+  std::vector<double> acc_stream_bytes, acc_stream_ms;
   int streams_used = 0;
   // migration
   cudaEvent_t mig_done_h2d = nullptr, mig_done_d2h = nullptr;
@@ -275,6 +277,12 @@ int harvest(ofb_runtime* rt, StepRecord* rec) {
     OFB_CUDA(cudaEventElapsedTime(&ms, c.start, c.stop));
     v.copy_sum += ms;
     v.copy_bytes += c.bytes;
+    if (static_cast<int>(rt->acc_stream_bytes.size()) <= c.stream) {
+      rt->acc_stream_bytes.resize(c.stream + 1, 0.0);
+      rt->acc_stream_ms.resize(c.stream + 1, 0.0);
+    }
+    rt->acc_stream_bytes[c.stream] += c.bytes;
+    rt->acc_stream_ms[c.stream] += ms;
     float a = 0, b = 0;
     OFB_CUDA(cudaEventElapsedTime(&a, rec->start, c.start));
     OFB_CUDA(cudaEventElapsedTime(&b, rec->start, c.stop));
@@ -895,12 +903,28 @@ int ofb_runtime_timing(ofb_runtime* rt, ofb_step_timing* out) {
   return 0;
 }
 
+int ofb_runtime_stream_stats(ofb_runtime* rt, int32_t max_streams, double* bytes, double* busy_ms,
+                             int32_t* streams) {
+  if (!rt) return fail(-1, "ofb_runtime_stream_stats: null runtime");
+  int rc = harvest_all(rt);
+  if (rc) return rc;
+  const int n = static_cast<int>(rt->acc_stream_bytes.size());
+  if (streams) *streams = n;
+  for (int i = 0; i < n && i < max_streams; ++i) {
+    if (bytes) bytes[i] = rt->acc_stream_bytes[i];
+    if (busy_ms) busy_ms[i] = rt->acc_stream_ms[i];
+  }
+  return 0;
+}
+
 int ofb_runtime_timing_reset(ofb_runtime* rt) {
   if (!rt) return fail(-1, "ofb_runtime_timing_reset: null runtime");
   int rc = harvest_all(rt);
   if (rc) return rc;
   rt->acc_steps = rt->acc_launches = 0;
   rt->acc_attn_ms = rt->acc_copy_bytes = rt->acc_step_ms = 0;
+  rt->acc_stream_bytes.clear();
+  rt->acc_stream_ms.clear();
   return 0;
 }
 

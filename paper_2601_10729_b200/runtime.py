@@ -80,6 +80,16 @@ class StepRuntime:
         _native.check(self.lib.ofb_runtime_timing(self.handle, ctypes.byref(t)), "ofb_runtime_timing")
         return {name: getattr(t, name) for name, _ in _native.StepTiming._fields_}
 
+    def stream_stats(self) -> list[dict]:
+        """Per copy stream: bytes fetched and busy ms over the timed steps."""
+        n = 64
+        b = (ctypes.c_double * n)()
+        t = (ctypes.c_double * n)()
+        k = ctypes.c_int32()
+        _native.check(self.lib.ofb_runtime_stream_stats(self.handle, n, b, t, ctypes.byref(k)),
+                      "ofb_runtime_stream_stats")
+        return [{"bytes": b[i], "busy_ms": t[i]} for i in range(min(k.value, n))]
+
     def timing_reset(self) -> None:
         _native.check(self.lib.ofb_runtime_timing_reset(self.handle), "ofb_runtime_timing_reset")
 
