@@ -183,6 +183,9 @@ class OprojAllReduce:
             raise ValueError(f"x must be contiguous [layers, batch, {self.k}]")
         if out is None:
             out = torch.empty((b, self.hidden), dtype=torch.bfloat16, device=x.device)
+        elif (out.shape != (b, self.hidden) or out.dtype != torch.bfloat16 or not out.is_contiguous()
+              or out.device != x.device):
+            raise ValueError(f"out must be a contiguous bf16 [{b}, {self.hidden}] tensor on {x.device}")
         d = _native.OprojDesc()
         d.x, d.w, d.out = x.data_ptr(), self.w.data_ptr(), out.data_ptr()
         d.layers, d.layer, d.batch, d.k, d.hidden = self.layers, layer, b, self.k, self.hidden
