@@ -49,3 +49,57 @@ def test_sm100a_sass_present():
     assert "UTMALDG" in sass          # TMA tile loads
     assert "HMMA" in sass             # tensor-core tiles of the GQA group
     assert "LDSM" in sass
+
+
+def test_sm100a_sass_has_tcgen05_in_k6():
+    """K6 issues 5th-gen tensor-core MMAs (UTCHMMA), reads the accumulator from
+    TMEM (LDTM) and stages operands with 3-D / 4-D TMA."""
+    from paper_2601_10729_b200 import build
+
+    path = build.build()
+    sass = subprocess.run(["cuobjdump", "-sass", str(path)], capture_output=True, text=True).stdout
+    for op in ("UTCHMMA", "LDTM", "UTMALDG.3D", "UTMALDG.4D"):
+        assert op in sass, op
+
+
+def test_k6_host_sizing_and_argument_errors():
+    """Host arithmetic and argument validation of the C1 entry points (no GPU)."""
+    import ctypes
+
+    from paper_2601_10729_b200 import _native
+
+    lib = _native.load()
+    # inbox [2][world][hidden][max_batch] bf16 (256-aligned) + flags [2][world][hidden/128] u32
+    inbox = 2 * 8 * 8192 * 32 * 2
+    assert lib.ofb_oproj_symm_bytes(8, 32, 8192) == (inbox + 255) // 256 * 256 + 2 * 8 * 64 * 4
+    assert lib.ofb_oproj_symm_bytes(9, 32, 8192) == -1          # world > 8
+    assert lib.ofb_oproj_symm_bytes(2, 0, 8192) == -1
+    assert lib.ofb_oproj_workspace_bytes(32, 1024, 8192) > 0
+    assert lib.ofb_oproj_workspace_bytes(32, 32, 8192) == -1      # k < 64
+
+    def call(**kw):
+        d = _native.OprojDesc()
+        d.x = d.w = d.out = d.workspace = 1 << 20
+        d.layers, d.layer, d.batch, d.k, d.hidden = 2, 0, 8, 128, 256
+        d.workspace_bytes = 256
+        d.world, d.rank, d.max_batch, d.epoch, d.w_layout = 1, 0, 8, 1, 1
+        for k, v in kw.items():
+            setattr(d, k, v)
+        rc = lib.ofb_oproj_allreduce(ctypes.byref(d), None)
+        return rc, lib.ofb_last_error().decode()
+
+    for bad, msg in [(dict(batch=9), "max_batch"), (dict(k=96), "multiple of 64"),
+                     (dict(hidden=200), "multiple of 128"), (dict(layer=2), "layer"),
+                     (dict(world=2, rank=0, epoch=0), "epoch"), (dict(w_layout=3), "w_layout"),
+                     (dict(world=9), "world")]:
+        rc, err = call(**bad)
+        assert rc == -1 and msg in err, (bad, rc, err)
+
+
+def test_runtime_calls_without_a_runtime_fail_cleanly():
+    from paper_2601_10729_b200 import _native
+
+    lib = _native.load()
+    assert lib.ofb_runtime_prefetch_fence(None, None) == -1
+    assert "null runtime" in lib.ofb_last_error().decode()
+    assert lib.ofb_runtime_step_layers(None, 1) == -1
