@@ -550,7 +550,7 @@ def run_ours(args, cfg):
                 "step_ms": [round(x, 3) for x in e2e_step_ms],
                 "prefetch_adopted_steps": pf1["adopted"] - pf0["adopted"],
                 "prefetch_dropped_steps": pf1["dropped"] - pf0["dropped"]},
-        "roofline": {"bound": "hbm", "kernel": "paged_gqa_decode_kernel (K1)",
+        "roofline": {"bound": "hbm", "kernel": "K1 paged GQA decode (paged_gqa_decode_stream_kernel: auto picks stream-K at this shape)",
                      "achieved": attn_gbs, "peak": hbm_peak, "unit": "GB/s",
                      "frac": attn_gbs / hbm_peak,
                      "traffic": (traffic or {}).get("bytes"),
