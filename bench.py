@@ -174,6 +174,12 @@ def _stream_summary(per_stream, nominal_gbs, peak_gbs):
             "bytes_per_stream": [s["bytes"] for s in per_stream][:16]}
 
 
+def _native_variant(batch, hkv, max_seq_len) -> int:
+    from paper_2601_10729_b200 import _native
+
+    return int(_native.load().ofb_attention_variant_for(batch, hkv, max_seq_len))
+
+
 def _mem_available() -> int:
     try:
         for line in open("/proc/meminfo"):
@@ -550,7 +556,9 @@ def run_ours(args, cfg):
                 "step_ms": [round(x, 3) for x in e2e_step_ms],
                 "prefetch_adopted_steps": pf1["adopted"] - pf0["adopted"],
                 "prefetch_dropped_steps": pf1["dropped"] - pf0["dropped"]},
-        "roofline": {"bound": "hbm", "kernel": "K1 paged GQA decode (paged_gqa_decode_stream_kernel: auto picks stream-K at this shape)",
+        "roofline": {"bound": "hbm", "kernel": ("K1 paged GQA decode (" + ("paged_gqa_decode_kernel, split variant"
+                                  if _native_variant(B, shape.num_kv_heads, int(tokens_per_layer / B))
+                                  else "paged_gqa_decode_stream_kernel, stream-K variant") + ")"),
                      "achieved": attn_gbs, "peak": hbm_peak, "unit": "GB/s",
                      "frac": attn_gbs / hbm_peak,
                      "traffic": (traffic or {}).get("bytes"),

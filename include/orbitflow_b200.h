@@ -44,6 +44,8 @@ OFB_API const char* ofb_last_error(void);
  * splits + last-CTA combine, 2 = auto (default: stream-K unless few (request,
  * kv head) pairs span the whole grid).  Returns the previous variant. */
 OFB_API int ofb_set_attention_kernel(int32_t variant);
+/* Which decomposition a launch of this shape would use now: 0 stream-K, 1 split. */
+OFB_API int ofb_attention_variant_for(int32_t batch, int32_t num_kv_heads, int32_t max_seq_len);
 /* Diagnostics: stream-K K1 launches write 6 globaltimer stamps per CTA (entry,
  * past the dependency wait, first tile ready, last tile consumed, exit, SM id)
  * into `device_buffer` (uint64 [448][6]); NULL switches tracing off. */

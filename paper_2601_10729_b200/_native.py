@@ -99,6 +99,7 @@ SIGNATURES = {
     "ofb_last_error": (ctypes.c_char_p, []),
     "ofb_set_attention_kernel": (ctypes.c_int, [c_i32]),
     "ofb_k1_trace": (ctypes.c_int, [c_vp]),
+    "ofb_attention_variant_for": (ctypes.c_int, [c_i32, c_i32, c_i32]),
     "ofb_device_info": (ctypes.c_int, [c_i32p, c_i32p]),
     "ofb_host_alloc": (c_vp, [c_i64]),
     "ofb_host_free": (ctypes.c_int, [c_vp]),

@@ -440,6 +440,10 @@ bool pdl_enabled() {
   return on == 1;
 }
 
+int attention_variant_for(int batch, int hkv, int max_seq_len) {
+  return use_split_kernel(batch, hkv, max_seq_len) ? 1 : 0;
+}
+
 int set_attention_variant(int variant) {
   const int prev = k1_variant();
   if (variant >= 0 && variant <= 2) g_k1_variant = variant;

@@ -33,6 +33,7 @@ cudaError_t launch_kv_append(const void* k_new, const void* v_new, void* pool,
                              cudaStream_t stream);
 int attention_occupancy();
 int set_attention_variant(int variant);
+int attention_variant_for(int batch, int hkv, int max_seq_len);
 void set_k1_trace_buffer(void* buf);
 cudaError_t launch_kv_prefill(const void* k, const void* v, const uint64_t* dst, int num_layers,
                               int tokens, int hkv, cudaStream_t stream);
@@ -339,6 +340,10 @@ const char* ofb_last_error(void) { return g_err.c_str(); }
 int ofb_set_attention_kernel(int32_t variant) {
   if (variant < 0 || variant > 2) return fail(-1, "variant must be 0 (stream-K), 1 (split) or 2 (auto)");
   return ofb::set_attention_variant(variant);
+}
+
+int ofb_attention_variant_for(int32_t batch, int32_t num_kv_heads, int32_t max_seq_len) {
+  return ofb::attention_variant_for(batch, num_kv_heads, max_seq_len);
 }
 
 int ofb_k1_trace(void* device_buffer) {
