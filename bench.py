@@ -681,6 +681,51 @@ def cfg3_setup(args):
     return trace, profile, slo, cfg
 
 
+def run_cfg3_policies(args):
+    """Config 3 trace under every policy the reference ships (src/policies.py:270-276),
+    each on the B200 executor in live mode (measured step time drives the clock):
+    the paper's policy comparison (TPOT / TBT attainment, throughput) on real steps."""
+    import torch
+
+    from paper_2601_10729_b200.engine import Simulation
+    from paper_2601_10729_b200.executor import B200Executor, LLAMA31_8B
+    from paper_2601_10729_b200.metrics import collect_metrics
+    from paper_2601_10729_b200.policies import PolicyKind, make_policy
+
+    trace, profile, slo, cfg = cfg3_setup(args)
+    rows = {}
+    for kind in PolicyKind:
+        policy = make_policy(kind, profile, slo, max_batch=cfg.max_batch, token_cap=cfg.batch_token_cap)
+        ex = B200Executor.for_trace(trace, profile, shape=LLAMA31_8B, max_batch=cfg.max_batch)
+        t0 = time.perf_counter()
+        try:
+            log = Simulation(trace, policy, profile, slo, cfg, executor=ex, mode="live").execute()
+        except Exception as exc:   # a policy the budget cannot serve: report, do not hide
+            rows[kind.value] = {"error": repr(exc)}
+            ex.close()
+            continue
+        wall = time.perf_counter() - t0
+        steps = [r for r in log if r["kind"] == "step"]
+        gpu_ms = sum(r["payload"]["measured_us"] for r in steps) / 1e3
+        tokens = sum(len(r["payload"]["ids"]) for r in steps)
+        rep = collect_metrics(log)
+        rows[kind.value] = {"steps": len(steps), "tokens": tokens, "gpu_ms": gpu_ms,
+                            "tokens_per_s_gpu": tokens / (gpu_ms * 1e-3) if gpu_ms else None,
+                            "makespan_ms": max((r["time_us"] for r in log), default=0) / 1e3,
+                            "throughput_rpm": rep.throughput_rpm, "tpot_p95_ms": rep.tpot_p95_ms,
+                            "tpot_attainment": rep.tpot_attainment,
+                            "tbt_attainment": rep.tbt_attainment, "tbt_p95_ms": rep.tbt_p95_ms,
+                            "pauses": rep.pauses, "replans": rep.replans,
+                            "preemptions": rep.preemptions,
+                            "h2d_migrated_bytes": ex.migrated["h2d_bytes"], "wall_s": wall}
+        ex.close()
+        torch.cuda.synchronize()
+        print(json.dumps({"policy": kind.value, **rows[kind.value]}), file=sys.stderr, flush=True)
+    print(json.dumps({"metric": METRIC, "config": "cfg3-policies", "mode": "live",
+                      "requests": len(trace.requests), "budget_blocks": profile.gpu_block_budget,
+                      "policies": rows}), flush=True)
+
+
 def run_cfg3(args):
     import torch
 
@@ -736,7 +781,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS) + ["cfg3", "cfg5"], default="cfg2")
+    ap.add_argument("--config", choices=sorted(CONFIGS) + ["cfg3", "cfg3-policies", "cfg5"],
+                    default="cfg2")
     ap.add_argument("--slo-scale", type=float, default=1.5)
     ap.add_argument("--cfg3-requests", type=int, default=10)
     ap.add_argument("--cfg3-output-median", type=int, default=48)
@@ -760,6 +806,8 @@ def main():
         return run_reconfig(args)
     if args.config == "cfg3":
         return run_cfg3(args)
+    if args.config == "cfg3-policies":
+        return run_cfg3_policies(args)
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference_arm(args, cfg)
