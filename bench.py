@@ -694,7 +694,10 @@ def run_cfg3_policies(args):
 
     trace, profile, slo, cfg = cfg3_setup(args)
     rows = {}
+    wanted = [k.strip() for k in args.cfg3_policies.split(",")] if args.cfg3_policies else None
     for kind in PolicyKind:
+        if wanted and kind.value not in wanted:
+            continue
         policy = make_policy(kind, profile, slo, max_batch=cfg.max_batch, token_cap=cfg.batch_token_cap)
         ex = B200Executor.for_trace(trace, profile, shape=LLAMA31_8B, max_batch=cfg.max_batch)
         t0 = time.perf_counter()
@@ -702,6 +705,7 @@ def run_cfg3_policies(args):
             log = Simulation(trace, policy, profile, slo, cfg, executor=ex, mode="live").execute()
         except Exception as exc:   # a policy the budget cannot serve: report, do not hide
             rows[kind.value] = {"error": repr(exc)}
+            print(json.dumps({"policy": kind.value, **rows[kind.value]}), file=sys.stderr, flush=True)
             ex.close()
             continue
         wall = time.perf_counter() - t0
@@ -787,6 +791,8 @@ def main():
     ap.add_argument("--cfg3-requests", type=int, default=10)
     ap.add_argument("--cfg3-output-median", type=int, default=48)
     ap.add_argument("--cfg3-budget-blocks", type=int, default=100000)
+    ap.add_argument("--cfg3-policies", default="",
+                    help="comma list for --config cfg3-policies (default: every policy)")
     ap.add_argument("--staging-slots", type=int, default=2,
                     help="1 = reference single-slot launch rule, 2 = double-buffered staging")
     ap.add_argument("--copy-streams", type=int, default=16)
