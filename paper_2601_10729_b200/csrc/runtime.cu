@@ -5,7 +5,9 @@
 // caller's compute stream.  One ofb_runtime_decode_step call enqueues a whole
 // step (1 append + L attention launches + every slab fetch) without blocking
 // the host, so the reference's Alg.-1 schedule (kvsim/latency.py:141-209) is
-// enforced by the GPU itself rather than simulated.
+// enforced by the GPU itself rather than simulated.  A step also enqueues the
+// next step's first fetches (cross-step prefetch), adopted by that step if its
+// transfer plan is unchanged, so the copy engines never wait for the host.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
