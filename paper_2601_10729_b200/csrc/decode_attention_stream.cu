@@ -11,6 +11,13 @@
 // CTAs; those write (O, lse) partials to per-CTA slots and the last CTA of the
 // pair to arrive (atomic ticket) combines them.  Pairs wholly inside one CTA
 // are written directly.
+//
+// Launched with programmatic dependent launch: everything before the
+// griddepcontrol.wait touches launch inputs only; with kv_ready (a layer with
+// no fetch this step, whose KV the host knows complete) the TMA producer also
+// starts streaming KV before the wait, so this layer's CTAs fill the SMs the
+// previous kernel's early finishers free.  ofb_k1_trace records per-CTA
+// timelines (tools/k1_trace.py).
 #include <cstddef>
 
 #include "attn_tile.cuh"
