@@ -383,3 +383,34 @@ def test_cross_step_prefetch_is_invisible():
         assert torch.equal(a, b)
     assert runs[False][1]["adopted"] == 0
     assert runs[True][1]["adopted"] >= 5, runs[True][1]
+
+
+def test_cross_step_prefetch_in_the_tensor_parallel_split_step():
+    """The per-layer split step (TP decoder: K1 + K6 per layer) adopts the cross-step
+    prefetch too; hidden states are bit-identical with and without it."""
+    from paper_2601_10729_b200.executor import ModelShape
+    from paper_2601_10729_b200.tp import HeadShard, TensorParallelDecoder
+
+    shape = ModelShape(4, 8, 2)
+    hiddens, stats = {}, {}
+    for prefetch in (False, True):
+        batch = [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=200 + 90 * i,
+                              target_output_tokens=16) for i in range(3)]
+        ex = _executor(shape, device_blocks=2000, host_blocks=2000, staging_slots=2, seed=4,
+                       prefetch_next=prefetch)
+        pm = PlacementMatrix.from_strides([0, 1, 2], 4, [2, 1, None])
+        ex.install(batch, pm)
+        tpd = TensorParallelDecoder(ex, HeadShard(0, 1, 8, 2), hidden=256, seed=2, max_batch=3)
+        out = []
+        for step in range(4):
+            out.append(tpd.step(batch, ex.synthetic_inputs(3, step=step)).clone())
+            for r in batch:
+                r.record_generated_token()
+        ex.drain()
+        hiddens[prefetch] = [h.cpu() for h in out]
+        stats[prefetch] = ex.runtime.prefetch_stats()
+        tpd.close()
+        ex.close()
+    for a, b in zip(hiddens[False], hiddens[True]):
+        assert torch.equal(a, b)
+    assert stats[True]["adopted"] == 3 and stats[False]["adopted"] == 0
