@@ -27,6 +27,7 @@
 // pushes, which come after this rank finished reading epoch e (stream order).
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -618,13 +619,19 @@ int ofb_oproj_allreduce(const ofb_oproj_desc* d, void* stream) {
   a.flags_off = static_cast<long long>((inbox_bytes(d->world, d->max_batch, d->hidden) + 255) / 256 * 256);
 
   const size_t smem = static_cast<size_t>(a.stages) * stage_bytes + red_bytes(splits, npad) + 1024;
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(oproj_allreduce_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSmemBudget + 2048));
-    if (e != cudaSuccess) return report_cuda(e, "cudaFuncSetAttribute(oproj_allreduce_kernel)");
-    configured = kSmemBudget + 2048;
+  {  // the dynamic-smem opt-in is per device: set it once for each device used
+    static std::mutex mu;
+    static std::vector<int> configured;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return report_cuda(e, "cudaGetDevice");
+    std::lock_guard<std::mutex> lock(mu);
+    if (std::find(configured.begin(), configured.end(), dev) == configured.end()) {
+      e = cudaFuncSetAttribute(oproj_allreduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(kSmemBudget + 2048));
+      if (e != cudaSuccess) return report_cuda(e, "cudaFuncSetAttribute(oproj_allreduce_kernel)");
+      configured.push_back(dev);
+    }
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(tiles * splits);
