@@ -805,7 +805,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tp-emulate", type=int, default=1,
                     help="run rank 0's KV-head shard of a TP-N deployment on one GPU")
-    ap.add_argument("--sweep-max-tokens", type=int, default=524288,
+    ap.add_argument("--sweep-max-tokens", type=int, default=1048576,
                     help="cfg5: largest B x T swept (KV bytes = tokens x 128 KiB)")
     args = ap.parse_args()
     if args.config == "cfg5":
