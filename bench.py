@@ -355,6 +355,9 @@ def run_ours(args, cfg):
     shard = HeadShard(rank if world > 1 else 0, tp, hq_total, hkv_total)
     shape = ModelShape(cfg["layers"], shard.local_q, shard.local_kv)
     L, B = cfg["layers"], cfg["batch"]
+    # every request must have tokens left for all the steps this run makes
+    # (warm-up, timed, instrumented, e2e warm-up + timed)
+    cfg = dict(cfg, output=max(cfg["output"], args.warmup + 2 * args.steps + 3 + 8 + 16))
     cap = -(-(cfg["prompt"] + cfg["output"] + 1) // 16)
     slots = args.staging_slots
     use_tp = world > 1 or args.tp_emulate > 1 or cfg["strides"] == "flexgen_plus"
