@@ -346,7 +346,8 @@ def test_reactive_preemption_releases_and_reprefills():
     ex.close()
 
 
-def test_cross_step_prefetch_is_invisible():
+@pytest.mark.parametrize("slots", [1, 2])
+def test_cross_step_prefetch_is_invisible(slots):
     """Each step enqueues the next step's first fetches (cross-step prefetch); the
     next step adopts them when its plan is unchanged and fences them otherwise.
     Outputs must be bit-identical to running without it, across a plan change
@@ -358,7 +359,7 @@ def test_cross_step_prefetch_is_invisible():
     for prefetch in (False, True):
         batch = [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=300 + 57 * i,
                               target_output_tokens=40) for i in range(3)]
-        ex = _executor(shape, device_blocks=4000, host_blocks=4000, staging_slots=2, seed=11,
+        ex = _executor(shape, device_blocks=4000, host_blocks=4000, staging_slots=slots, seed=11,
                        prefetch_next=prefetch)
         pm = PlacementMatrix.from_strides([0, 1, 2], 6, [2, 1, None])
         ex.install(batch, pm)
