@@ -366,7 +366,17 @@ def run_ours(args, cfg):
     oproj_bytes = L * shard.local_q * 128 * cfg["hidden"] * 2 if use_tp else 0
     staging_bytes = B * slots * cap * shape.block_bytes
     kv_budget = free_b - oproj_bytes - staging_bytes - (6 << 30)
+    if dist is not None:
+        # C2: every rank must plan with the same budget - the smallest
+        t = torch.tensor([kv_budget], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        kv_budget = int(t.item())
     batch, placement = build_batch(cfg, shape, kv_budget)
+    if dist is not None:
+        from paper_2601_10729_b200.tp import check_plan_replicated
+
+        if not check_plan_replicated(placement.rows):
+            raise SystemExit("ranks computed different placements (C2 violated)")
     n_off = sum(row.count(0) for row in placement.rows)
     n_res = L * B - n_off
     host_need = n_off * cap * shape.block_bytes
