@@ -688,7 +688,12 @@ def cfg3_setup(args):
     trace = workload.Trace(tuple(workload.TraceRequest(r.arrival_ms, max(r.prompt_tokens, 8192),
                                                        r.output_tokens) for r in raw.requests),
                            dict(raw.metadata, min_prompt="8192"))
-    profile = b200_profile(32, 8, gpu_block_budget=args.cfg3_budget_blocks)
+    if args.cfg3_calibrate:   # price with this box's measured K1 / link
+        from paper_2601_10729_b200.calibrate import measure_b200_profile
+
+        profile, _raw = measure_b200_profile(32, 32, 8, args.cfg3_budget_blocks)
+    else:
+        profile = b200_profile(32, 8, gpu_block_budget=args.cfg3_budget_blocks)
     slo = defaults.default_slo(profile, scale=args.slo_scale)
     cfg = RunConfig(max_batch=4, batch_token_cap=600000)
     return trace, profile, slo, cfg
@@ -766,7 +771,12 @@ def run_cfg3(args):
            "workload": "Llama-3.1-8B shape, mixed 8K-128K lognormal trace (seed 3), OrbitPolicy, "
                        f"max_batch 4, HBM budget {profile.gpu_block_budget} blocks x 64 KiB",
            "requests": len(trace.requests),
-           "prompts": [r.prompt_tokens for r in trace.requests]}
+           "prompts": [r.prompt_tokens for r in trace.requests],
+           "profile": {"source": "measured on this GPU" if args.cfg3_calibrate
+                       else "round-1 B200 constants (calibrate.py)",
+                       "compute_base_ms": profile.compute_base_ms,
+                       "compute_per_token_ms": profile.compute_per_token_ms,
+                       "bandwidth_blocks_per_ms": profile.bandwidth_blocks_per_ms}}
     steps_model = [r for r in model_log if r["kind"] == "step"]
     out["host_control_ms_per_step"] = model_s * 1e3 / max(1, len(steps_model))
     for mode in ("parity", "live"):
@@ -804,6 +814,8 @@ def main():
     ap.add_argument("--cfg3-requests", type=int, default=10)
     ap.add_argument("--cfg3-output-median", type=int, default=48)
     ap.add_argument("--cfg3-budget-blocks", type=int, default=100000)
+    ap.add_argument("--cfg3-calibrate", action="store_true",
+                    help="cfg3: SystemProfile measured on this GPU (K1 slope/intercept, link)")
     ap.add_argument("--cfg3-policies", default="",
                     help="comma list for --config cfg3-policies (default: every policy)")
     ap.add_argument("--staging-slots", type=int, default=2,

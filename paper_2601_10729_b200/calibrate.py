@@ -40,3 +40,62 @@ def b200_profile(num_layers: int, num_kv_heads: int, gpu_block_budget: int, *,
         block_size=block_size,
         prefill_per_token_ms=prefill_per_token_ms,
     )
+
+
+def measure_b200_profile(num_layers: int, num_q_heads: int, num_kv_heads: int,
+                         gpu_block_budget: int, *, batch: int = 16,
+                         contexts: tuple[int, int] = (2048, 16384), iters: int = 10,
+                         device=None) -> tuple[SystemProfile, dict]:
+    """Calibrate the cost model on this GPU instead of using the round-1 constants
+    (SURVEY.md H4): time K1 (CUDA events, back-to-back launches) on synthetic paged
+    KV at two context lengths - slope -> ``compute_per_token_ms``, intercept ->
+    ``compute_base_ms`` - and probe the pinned host link (best-of-10 1 GiB H2D) for
+    ``bandwidth_blocks_per_ms``.  Returns the profile and the raw measurements."""
+    import statistics
+
+    import torch
+
+    from . import _native, ops
+    from .runtime import link_probe
+
+    dev = torch.device(device if device is not None else "cuda")
+    times = {}
+    for ctx in contexts:
+        nblk = (ctx + 15) // 16
+        pools = [torch.empty((batch * nblk, num_kv_heads, 2, 16, 128), dtype=torch.bfloat16,
+                             device=dev).normal_() for _ in range(2)]
+        bt = torch.arange(batch * nblk, dtype=torch.int32, device=dev).reshape(batch, nblk)
+        lens = torch.full((batch,), ctx, dtype=torch.int32, device=dev)
+        q = torch.randn((batch, num_q_heads, 128), device=dev).to(torch.bfloat16)
+        out = torch.empty_like(q)
+        ws = ops.workspace(batch, num_q_heads, num_kv_heads, ctx, dev)
+        for p in pools:
+            ops.decode_attention(q, p, bt, lens, out=out, max_seq_len=ctx, ws=ws)
+        torch.cuda.synchronize()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(iters + 1)]
+        evs[0].record()
+        for i in range(iters):
+            ops.decode_attention(q, pools[i % 2], bt, lens, out=out, max_seq_len=ctx, ws=ws)
+            evs[i + 1].record()
+        torch.cuda.synchronize()
+        times[ctx] = statistics.median(evs[i].elapsed_time(evs[i + 1]) for i in range(iters))
+        del pools
+    (c0, t0), (c1, t1) = sorted(times.items())
+    per_token = (t1 - t0) / ((c1 - c0) * batch)          # ms per cached token per layer
+    base = max(t0 - per_token * c0 * batch, 0.0)
+    lib = _native.load()
+    nbytes = 1 << 30
+    host = lib.ofb_host_alloc(nbytes)
+    if not host:
+        raise RuntimeError("pinned probe buffer allocation failed")
+    try:
+        d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        h2d, d2h = link_probe(host, d.data_ptr(), nbytes, 10)
+    finally:
+        lib.ofb_host_free(host)
+    kv_bytes_per_token = num_kv_heads * 2 * 128 * 2
+    k1_gbs = kv_bytes_per_token / (per_token * 1e6)
+    prof = b200_profile(num_layers, num_kv_heads, gpu_block_budget, k1_gbs=k1_gbs, h2d_gbs=h2d,
+                        layer_fixed_ms=base)
+    return prof, {"k1_ms": times, "k1_gbs_slope": k1_gbs, "layer_fixed_ms": base,
+                  "h2d_gbs": h2d, "d2h_gbs": d2h}

@@ -415,3 +415,16 @@ def test_cross_step_prefetch_in_the_tensor_parallel_split_step():
     for a, b in zip(hiddens[False], hiddens[True]):
         assert torch.equal(a, b)
     assert stats[True]["adopted"] == 3 and stats[False]["adopted"] == 0
+
+
+def test_live_calibration_of_the_cost_model():
+    """the SystemProfile the planner prices with can be measured on the
+    box (K1 slope / intercept, pinned link) instead of taken from constants."""
+    from paper_2601_10729_b200.calibrate import measure_b200_profile
+
+    prof, raw = measure_b200_profile(32, 32, 8, 100_000, batch=8, contexts=(1024, 8192), iters=5)
+    assert 3000 < raw["k1_gbs_slope"] < 9000, raw
+    assert 0.0 <= raw["layer_fixed_ms"] < 0.1, raw
+    assert 30 < raw["h2d_gbs"] < 70, raw
+    assert prof.num_layers == 32 and prof.gpu_block_budget == 100_000
+    assert prof.bandwidth_blocks_per_ms == pytest.approx(raw["h2d_gbs"] * 1e6 / 65536)
