@@ -790,7 +790,8 @@ def run_cfg3(args):
                "tokens_per_s_gpu": tokens / (gpu_ms * 1e-3), "wall_s": wall_s,
                "tpot_attainment": rep.tpot_attainment, "tbt_attainment": rep.tbt_attainment,
                "tbt_p95_ms": rep.tbt_p95_ms, "pauses": rep.pauses, "resumes": rep.resumes,
-               "replans": rep.replans, "migrated": dict(ex.migrated)}
+               "replans": rep.replans, "migrated": dict(ex.migrated),
+               "prefetch": ex.runtime.prefetch_stats()}
         if mode == "parity":
             stripped = [dict(r, payload={k: v for k, v in r["payload"].items() if k != "measured_us"})
                         if r["kind"] == "step" else r for r in log]

@@ -190,11 +190,31 @@ class B200Executor:
             self.slabs[req.id] = st
         return st
 
+    def _table_differs(self, table, reqs) -> bool:
+        """True if making residency equal ``table.locations`` moves anything."""
+        if any(rid not in table.locations for rid in self.slabs):
+            return True
+        for rid, locs in table.locations.items():
+            if rid not in reqs:
+                continue
+            st = self.slabs.get(rid)
+            if st is None:
+                return True
+            if any((loc in _DEVICE_LOCS) != (st.dev[l] is not None) for l, loc in enumerate(locs)):
+                return True
+        return False
+
     def sync_table(self, table, batch, paused=()) -> None:
-        """Migrate slabs so physical residency equals ``table.locations``."""
+        """Migrate slabs so physical residency equals ``table.locations``.
+
+        The engine re-installs its plan at every step boundary (src/engine.py:
+        708-713); when nothing moves this is a no-op, so the layout (and the
+        cross-step prefetch the previous step issued) stays valid."""
+        reqs = {r.id: r for r in [*batch, *paused]}
+        if not self._table_differs(table, reqs):
+            return
         # no staging slot or host slab may be reused under an in-flight prefetch
         self.runtime.prefetch_fence()
-        reqs = {r.id: r for r in [*batch, *paused]}
         for rid in [r for r in self.slabs if r not in table.locations]:
             self.release(rid)
         moves, evicted = [], []
