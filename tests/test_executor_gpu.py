@@ -428,3 +428,25 @@ def test_live_calibration_of_the_cost_model():
     assert 30 < raw["h2d_gbs"] < 70, raw
     assert prof.num_layers == 32 and prof.gpu_block_budget == 100_000
     assert prof.bandwidth_blocks_per_ms == pytest.approx(raw["h2d_gbs"] * 1e6 / 65536)
+
+
+@pytest.mark.parametrize("hq,hkv", [(16, 1), (4, 4), (64, 8)])
+def test_full_step_other_head_layouts(hq, hkv):
+    """The whole step (K3 append, K2 fetches, K1) for GQA group 16, MHA (group 1)
+    and the 70B head layout, vs the oracle on every (layer, request)."""
+    from paper_2601_10729_b200.executor import ModelShape
+
+    shape = ModelShape(4, hq, hkv)
+    batch = [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=130 + 77 * i,
+                          target_output_tokens=8) for i in range(3)]
+    pm = PlacementMatrix.from_strides([0, 1, 2], 4, [2, None, 1])
+    ex = _executor(shape, device_blocks=400, host_blocks=400, staging_slots=2, seed=hq + hkv)
+    try:
+        ex.install(batch, pm)
+        for _ in range(2):
+            ex.decode_step(batch, pm)
+            _check_step_outputs(ex, batch)
+            for r in batch:
+                r.record_generated_token()
+    finally:
+        ex.close()
