@@ -292,6 +292,8 @@ typedef struct ofb_plan_problem {
   const double* forecast_live;    /* [batch] */
   const double* forecast_parked;  /* [num_paused] */
   int32_t* strides_out;           /* [batch] chosen stride, -1 = resident */
+  int32_t device_enumerate;       /* 1: enumerate + sort the candidate space on the GPU
+                                     (same order, same plan; needs a CUDA device) */
 } ofb_plan_problem;
 
 typedef struct ofb_plan_result {

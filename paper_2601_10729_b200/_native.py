@@ -68,7 +68,7 @@ class PlanProblem(ctypes.Structure):
         ("mode", c_i32), ("threads", c_i32),
         ("total_tokens", c_vp), ("blocks", c_vp), ("live_balance", c_vp),
         ("parked_balance", c_vp), ("forecast_live", c_vp), ("forecast_parked", c_vp),
-        ("strides_out", c_vp),
+        ("strides_out", c_vp), ("device_enumerate", c_i32),
     ]
 
 

@@ -25,11 +25,20 @@
 #include <functional>
 #include <numeric>
 #include <queue>
+#include <stdexcept>
 #include <string>
 #include <thread>
 #include <vector>
 
 #include "../../include/orbitflow_b200.h"
+
+namespace ofb {
+int plan_gpu_enumerate(int B, int C, int L, const int* count, const uint8_t* mask,
+                       const int64_t* blocks, int64_t budget, double compL, double bw,
+                       void** handle, int64_t* n_feasible, std::string* err);
+int plan_gpu_fetch(void* handle, int64_t from, int64_t count, uint64_t* dst, std::string* err);
+void plan_gpu_free(void* handle);
+}  // namespace ofb
 
 namespace {
 
@@ -374,8 +383,12 @@ void parallel_for(int64_t n, int threads, Fn fn) {
 struct Ranker {
   const Problem& P;
   int B, threads;
-  std::vector<Cand> cands;        // capacity-feasible, in lower-bound order
+  std::vector<Cand> cands;        // capacity-feasible, in lower-bound order (a prefix
+                                  // when the list lives on the GPU, pulled in chunks)
   std::vector<double> lb;
+  int64_t total = 0;              // feasible candidates in all
+  void* gpu = nullptr;            // device-sorted candidate list (build_gpu)
+  ~Ranker() { ofb::plan_gpu_free(gpu); }
   size_t priced = 0;
   std::vector<Ranked> heap;       // min-heap of priced, unreleased candidates
   int64_t n_priced = 0;
@@ -498,7 +511,45 @@ struct Ranker {
     }
     lb.resize(n);
     for (size_t i = 0; i < n; ++i) lb[i] = std::max(compL, (double)cands[i].fetch / bw);
+    total = (int64_t)n;
     return true;
+  }
+
+  // Same list, enumerated and sorted on the GPU (planner_gpu.cu); the host keeps
+  // only the prefix the ranking has reached.
+  bool build_gpu() {
+    const Options& op = P.op;
+    const double compL = P.comp * (double)op.L;
+    std::string err;
+    if (ofb::plan_gpu_enumerate(B, op.C, op.L, op.count.data(), op.mask.data(), P.p->blocks,
+                                P.p->gpu_block_budget, compL, P.p->bandwidth_blocks_per_ms,
+                                &gpu, &total, &err) != 0)
+      throw std::runtime_error(err);
+    if (total == 0) return false;
+    pull();
+    return true;
+  }
+
+  static constexpr int64_t kPull = 1 << 20;
+
+  void pull() {   // next chunk of the GPU-sorted list
+    const int64_t from = (int64_t)cands.size();
+    const int64_t n = std::min(kPull, total - from);
+    if (n <= 0) return;
+    std::vector<uint64_t> keys((size_t)n);
+    std::string err;
+    if (ofb::plan_gpu_fetch(gpu, from, n, keys.data(), &err) != 0) throw std::runtime_error(err);
+    const Options& op = P.op;
+    const double compL = P.comp * (double)op.L, bw = P.p->bandwidth_blocks_per_ms;
+    int pick[64];
+    for (uint64_t k : keys) {
+      const int64_t idx = (int64_t)(k & 0xffffffffull);
+      decode(idx, op.C, B, pick);
+      int64_t fetch = 0;
+      for (int r = 0; r < B; ++r) fetch += P.p->blocks[r] * op.count[pick[r]];
+      cands.push_back({idx, fetch});
+      lb.push_back(std::max(compL, (double)fetch / bw));
+    }
   }
 
   void price_chunk() {
@@ -532,9 +583,11 @@ struct Ranker {
   bool next(Ranked* out) {
     auto greater = [&](const Ranked& a, const Ranked& b) { return rank_less(P.op, B, b, a); };
     while (true) {
+      if (priced >= cands.size() && (int64_t)cands.size() < total) pull();
       bool drained = priced >= cands.size();
       if (!drained && hopeless && hopeless(lb[priced])) {
         cands.resize(priced);  // nothing past here can pass: stop pricing
+        total = (int64_t)priced;
         drained = true;
       }
       if (!heap.empty() && (drained || heap.front().lat + kRankEps < lb[priced])) {
@@ -566,31 +619,7 @@ extern "C" {
 
 const char* ofb_plan_last_error(void) { return g_plan_err.c_str(); }
 
-int ofb_plan_solve(const ofb_plan_problem* p, ofb_plan_result* out) {
-  if (!p || !out) {
-    g_plan_err = "null argument";
-    return -1;
-  }
-  std::memset(out, 0, sizeof(*out));
-  if (p->batch < 1 || p->batch > 12 || p->num_layers < 1 || p->num_paused < 0 ||
-      p->num_paused > 64) {
-    g_plan_err = "batch must be 1..12 and num_layers >= 1";
-    return -1;
-  }
-  Problem P(p);
-  int64_t space = 1;
-  for (int r = 0; r < p->batch; ++r) space *= P.op.C;
-  if (space > (int64_t)1 << 28) {
-    g_plan_err = "candidate space too large for exhaustive search";
-    return -1;
-  }
-  const int threads = std::max(1, p->threads);
-  Ranker rk(P, threads);
-  if (!rk.build()) {
-    out->status = 1;  // no placement fits the GPU block budget
-    return 0;
-  }
-  out->candidates_feasible = (int64_t)rk.cands.size();
+static int solve_ranked(const ofb_plan_problem* p, const Problem& P, Ranker& rk, ofb_plan_result* out) {
   int pick[64];
   std::vector<int> fails;
   const int B = p->batch;
@@ -644,6 +673,47 @@ int ofb_plan_solve(const ofb_plan_problem* p, ofb_plan_result* out) {
   out->candidates_priced = rk.n_priced;
   out->status = 0;
   return 0;
+}
+
+
+int ofb_plan_solve(const ofb_plan_problem* p, ofb_plan_result* out) {
+  if (!p || !out) {
+    g_plan_err = "null argument";
+    return -1;
+  }
+  std::memset(out, 0, sizeof(*out));
+  if (p->batch < 1 || p->batch > 12 || p->num_layers < 1 || p->num_paused < 0 ||
+      p->num_paused > 64) {
+    g_plan_err = "batch must be 1..12 and num_layers >= 1";
+    return -1;
+  }
+  Problem P(p);
+  int64_t space = 1;
+  for (int r = 0; r < p->batch; ++r) space *= P.op.C;
+  if (space > (int64_t)1 << 28) {
+    g_plan_err = "candidate space too large for exhaustive search";
+    return -1;
+  }
+  const int threads = std::max(1, p->threads);
+  Ranker rk(P, threads);
+  bool any = false;
+  try {
+    any = p->device_enumerate ? rk.build_gpu() : rk.build();
+  } catch (const std::exception& e) {
+    g_plan_err = e.what();
+    return -1;
+  }
+  if (!any) {
+    out->status = 1;  // no placement fits the GPU block budget
+    return 0;
+  }
+  out->candidates_feasible = rk.total;
+  try {
+    return solve_ranked(p, P, rk, out);
+  } catch (const std::exception& e) {   // a GPU chunk pull failed
+    g_plan_err = e.what();
+    return -1;
+  }
 }
 
 }  // extern "C"

@@ -86,3 +86,57 @@ def test_native_is_faster_at_b5():
     planner.SOLVER = "native"
     assert _plan_sig(a) == _plan_sig(b)
     assert t_native < t_py
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("L,B,count", [(4, 4, 30), (9, 3, 30), (32, 4, 6), (32, 5, 3)])
+def test_gpu_enumeration_matches_host(L, B, count):
+    """SOLVER="native-gpu" (candidate space enumerated + radix-sorted on the GPU)
+    returns exactly the host solver's plans, windows and latencies."""
+    rng = random.Random(1000 + L * 10 + B)
+    for _ in range(count):
+        batch, prof, slo, paused, snap = _instance(rng, L, B)
+        for cap_only in (False, True):
+            def run():
+                if cap_only:
+                    return _plan_sig(planner.solve_capacity_only(batch, prof, slo, 3))
+                return _plan_sig(planner.solve(batch, prof, slo, 3, paused=paused,
+                                               deposit_snapshot=snap))
+            old = planner.SOLVER
+            try:
+                planner.SOLVER = "native"
+                a = run()
+                planner.SOLVER = "native-gpu"
+                b = run()
+            finally:
+                planner.SOLVER = old
+            assert a == b
+
+
+@pytest.mark.gpu
+def test_gpu_enumeration_b8_l32():
+    """B=8 at L=32 (214 M candidates; the reference is intractable here): the GPU
+    enumeration returns the host solver's plan, much faster."""
+    from paper_2601_10729_b200 import defaults
+    from paper_2601_10729_b200.calibrate import b200_profile
+
+    rng = random.Random(8)
+    prof = b200_profile(32, 8, gpu_block_budget=60000 * 8 // 4)
+    batch = [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=rng.randint(2000, 30000),
+                          target_output_tokens=64) for i in range(8)]
+    slo = defaults.default_slo(prof, 60.0)
+    old = planner.SOLVER
+    try:
+        planner.SOLVER = "native"
+        t = time.perf_counter()
+        a = _plan_sig(planner.solve(batch, prof, slo, 1))
+        t_host = time.perf_counter() - t
+        planner.SOLVER = "native-gpu"
+        planner.solve(batch, prof, slo, 1)            # warm-up (context, cub)
+        t = time.perf_counter()
+        b = _plan_sig(planner.solve(batch, prof, slo, 1))
+        t_gpu = time.perf_counter() - t
+    finally:
+        planner.SOLVER = old
+    assert a == b
+    assert t_gpu < t_host, (t_gpu, t_host)

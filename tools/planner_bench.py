@@ -38,6 +38,19 @@ for B in range(1, 9):
     t = time.perf_counter(); p_nat = planner.solve(batch, prof, slo, 1)
     rec["native_ms"] = (time.perf_counter() - t) * 1e3
     rec["plan"] = sig(p_nat)[0] if sig(p_nat)[0] == "infeasible" else [r.count(0) for r in p_nat.placement.rows]
+    rec["native_stats"] = planner.LAST_NATIVE_STATS
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            planner.SOLVER = "native-gpu"
+            planner.solve(batch, prof, slo, 1)             # warm-up (context, cub)
+            t = time.perf_counter(); p_gpu = planner.solve(batch, prof, slo, 1)
+            rec["native_gpu_ms"] = (time.perf_counter() - t) * 1e3
+            rec["native_gpu_equal"] = sig(p_gpu) == sig(p_nat)
+            planner.SOLVER = "native"
+    except ImportError:
+        pass
     if B <= 6:
         planner.SOLVER = "python"
         t = time.perf_counter(); p_py = planner.solve(batch, prof, slo, 1)
