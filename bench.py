@@ -293,7 +293,8 @@ def run_reference_arm(args, cfg):
     if rank != 0:
         return
     shape = ModelShape(cfg["layers"], cfg["hq"], cfg["hkv"])
-    batch, _placement = build_batch(cfg)
+    # the CPU arm attends every layer of host-resident KV: no placement needed
+    batch, _placement = build_batch(dict(cfg, strides=[None] * cfg["batch"]))
     per_layer = []
     sampler = CpuAttentionSample(shape, batch)
     threads = sampler.threads
