@@ -1,3 +1,6 @@
+"""Are per-CTA (per-SM) K1 streaming rates stable across launches?  Six traced
+launches on the same CTA->SM mapping: correlation of per-CTA and per-SM rates
+(profiles/r01_summary.md: ~0.3, i.e. mostly transient contention)."""
 import sys, json, numpy as np, torch
 sys.path.insert(0, "/root/repo")
 from paper_2601_10729_b200 import _native, ops

@@ -1,3 +1,5 @@
+"""One K6 launch of a given (batch, k, hidden) for compute-sanitizer runs
+(e.g. OFB_K6_SPLITS=8 compute-sanitizer --tool synccheck python tools/k6_sync_case.py 32 1024 2048)."""
 import sys, torch
 sys.path.insert(0, "/root/repo")
 from paper_2601_10729_b200.collective import OprojAllReduce
