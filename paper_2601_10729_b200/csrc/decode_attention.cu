@@ -298,9 +298,9 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
   if (single) return;
 
   // ------------------------------------------- last CTA combines the splits
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
+  __syncthreads();        // every partial write of the CTA happens-before thread 0's
+  if (tid == 0) {         // gpu-scope fence + ticket (cumulative release)
+    __threadfence();
     const int ticket = atomicAdd(&a.counters[req * a.hkv + kvh], 1);
     *flag = (ticket == nsplit - 1);
   }
@@ -337,7 +337,15 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
     const size_t qrow = (size_t)req * a.hq + qh0 + row;
     const float* src = a.ws_o + qrow * a.max_splits * kHeadDim + d;
     float acc = 0.f;
-    for (int s2 = 0; s2 < nsplit; ++s2) acc += wts[row * kMaxSplits + s2] * __ldcg(src + (size_t)s2 * kHeadDim);
+    int s2 = 0;
+    for (; s2 + 8 <= nsplit; s2 += 8) {   // 8 partial loads in flight, then the FMAs in order
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (size_t)(s2 + u) * kHeadDim);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += wts[row * kMaxSplits + s2 + u] * v[u];
+    }
+    for (; s2 < nsplit; ++s2) acc += wts[row * kMaxSplits + s2] * __ldcg(src + (size_t)s2 * kHeadDim);
     a.out[qrow * kHeadDim + d] = __float2bfloat16(acc * inv[row]);
   }
   if (tid == 0) a.counters[req * a.hkv + kvh] = 0;  // re-arm for the next launch
