@@ -46,6 +46,7 @@ struct AttnArgs {
   int hq, hkv, group;
   int blocks_per_split, max_splits;
   float scale_log2;
+  int kv_ready;                 // 1: KV complete before the PDL wait (see the stream kernel)
 };
 
 struct MergeScratch {
@@ -72,7 +73,12 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
   const int warp = tid >> 5;
   const int lane = tid & 31;
 
-  pdl_wait();     // see decode_attention_stream.cu: predecessor must be complete
+  // see decode_attention_stream.cu: the predecessor must be complete before q,
+  // outputs or workspace are touched; with kv_ready (host-guaranteed) the
+  // launch inputs and this layer's KV may be read - and the producer stream it -
+  // while the predecessor drains
+  const bool early = a.kv_ready != 0;
+  if (!early) pdl_wait();
   pdl_trigger();
   const int seq = a.seq_lens[req];
   const int nblk = (seq + kBlockTokens - 1) / kBlockTokens;
@@ -81,6 +87,7 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
   const int qh0 = kvh * g;
 
   if (nblk == 0) {  // empty request: defined output
+    if (early) pdl_wait();
     if (split == 0) {
       for (int i = tid; i < g * kHeadDim; i += kAttnThreads)
         a.out[((size_t)req * a.hq + qh0) * kHeadDim + i] = __float2bfloat16(0.f);
@@ -133,6 +140,7 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
     }
   } else {
     // ---------------------------------------------------------- consumers
+    if (early) pdl_wait();
     // Q as the A operand (rows = query heads of this group, zero padded).
     uint32_t qa[8][4];
     {
@@ -296,6 +304,7 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
     }
   }
   if (single) return;
+  if (early) pdl_wait();   // the producer warp joins the combine below
 
   // ------------------------------------------- last CTA combines the splits
   __syncthreads();        // every partial write of the CTA happens-before thread 0's
@@ -517,6 +526,7 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
   a.blocks_per_split = plan.blocks_per_split;
   a.max_splits = ws_splits;
   a.scale_log2 = scale * 1.4426950408889634f;
+  a.kv_ready = kv_ready ? 1 : 0;
   dim3 grid(plan.max_splits, hkv, batch);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
