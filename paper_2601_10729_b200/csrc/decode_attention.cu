@@ -396,24 +396,31 @@ static AttnPlan plan_splits(int batch, int hkv, int max_seq_len) {
   const int nblk = (max_seq_len + kBlockTokens - 1) / kBlockTokens;
   AttnPlan p{1, 1};
   if (nblk <= 0) return p;
-  const long slots = (long)g_num_sms * g_attn_occupancy;
   const long pairs = (long)batch * hkv;
   int lo = (nblk + kMaxSplits - 1) / kMaxSplits;
   lo = lo < 1 ? 1 : lo;
   int hi = nblk < kMaxBlocksPerSplit ? nblk : kMaxBlocksPerSplit;
   if (lo > hi) lo = hi;
-  double best = 1e300;
-  for (int bps = lo; bps <= hi; ++bps) {
-    const long splits = (nblk + bps - 1) / bps;
-    const long ctas = pairs * splits;
-    const long waves = (ctas + slots - 1) / slots;
-    // per-CTA fixed cost ~ 3 blocks of streaming (pipeline fill + merge),
-    // plus the combine pass reading `splits` partials when split.
-    const double cost = (double)waves * (bps + 3.0) + (splits > 1 ? 0.05 * splits : 0.0);
-    if (cost < best - 1e-9) {
-      best = cost;
-      p.blocks_per_split = bps;
-    }
+  // Each split costs a partial write and a longer combine; short splits are
+  // latency-bound, so fill each SM once rather than both CTA slots
+  // (tools/k1_overhead.py with OFB_K1_BPS: B=1, 8 KV heads, 4K / 16K / 64K
+  // tokens best at ~16 / ~16 / ~32 splits).
+  // One CTA per SM (never more CTAs than SMs: a doubled-up SM finishes last);
+  // long splits use both resident CTA slots, where the second CTA's stream adds
+  // bandwidth that outweighs the longer combine.
+  long splits = g_num_sms / pairs;
+  splits = splits < 1 ? 1 : splits;
+  if ((nblk + splits - 1) / splits >= 128) {
+    const long two = (long)g_num_sms * g_attn_occupancy / pairs;
+    splits = two > splits ? two : splits;
+  }
+  int bps = (int)((nblk + splits - 1) / splits);
+  if (bps < 8) bps = 8;   // a split must amortise its partial and its combine share
+  bps = bps < lo ? lo : (bps > hi ? hi : bps);
+  p.blocks_per_split = bps;
+  if (const char* f = std::getenv("OFB_K1_BPS")) {   // tuning experiments only
+    const int v = std::atoi(f);
+    if (v >= lo && v <= hi) p.blocks_per_split = v;
   }
   p.max_splits = (nblk + p.blocks_per_split - 1) / p.blocks_per_split;
   return p;
