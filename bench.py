@@ -203,8 +203,9 @@ def _ncu_traffic(alg_bytes):
     from paper_2601_10729_b200 import ops
 
     paths = sorted((ROOT / "profiles").glob("*ncu_full_cfg2layer.json"), reverse=True)
-    # the capture of the K1 variant that auto-selection runs at this shape first
-    paths.sort(key=lambda p: ("stream" not in p.name))
+    # the capture of the K1 variant that runs at this shape first
+    split = bool(_native_variant(16, 8, 32768))
+    paths.sort(key=lambda p: (("k1split" in p.name) != split))
     for path in paths:
         try:
             rec = json.loads(path.read_text())[0]

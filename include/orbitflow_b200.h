@@ -41,8 +41,8 @@ extern "C" {
 OFB_API const char* ofb_version(void);
 OFB_API const char* ofb_last_error(void);
 /* K1 work decomposition for later launches: 0 = persistent stream-K, 1 = fixed
- * splits + last-CTA combine, 2 = auto (default: stream-K unless few (request,
- * kv head) pairs span the whole grid).  Returns the previous variant. */
+ * splits + last-CTA combine, 2 = auto (default: the split kernel, which with its
+ * current plan wins on every measured shape).  Returns the previous variant. */
 OFB_API int ofb_set_attention_kernel(int32_t variant);
 /* Which decomposition a launch of this shape would use now: 0 stream-K, 1 split. */
 OFB_API int ofb_attention_variant_for(int32_t batch, int32_t num_kv_heads, int32_t max_seq_len);

@@ -449,10 +449,15 @@ static int k1_variant() {
   return g_k1_variant;
 }
 
+// Auto = split: with the split plan below (one CTA per SM, both slots only for
+// long splits) the split kernel beat stream-K on every shape of
+// profiles/r01_k1_sweep.md (B 1-32, 4K-64K, 8B / 70B / TP8-shard heads) and in
+// the cfg2 / cfg2r / cfg4 steps; stream-K stays selectable (variant 0).
 static bool use_split_kernel(int batch, int hkv, int max_seq_len) {
-  const int v = k1_variant();
-  if (v == 2) return !stream_preferred(batch, hkv, max_seq_len);
-  return v == 1;
+  (void)batch;
+  (void)hkv;
+  (void)max_seq_len;
+  return k1_variant() != 0;
 }
 
 bool pdl_enabled() {
