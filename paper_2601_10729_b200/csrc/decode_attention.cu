@@ -340,22 +340,74 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
     if (lane == 0) inv[row] = 1.f / S;
   }
   __syncthreads();
-  for (int idx = tid; idx < g * kHeadDim; idx += kAttnThreads) {
-    const int row = idx / kHeadDim;
-    const int d = idx - row * kHeadDim;
+  // The combine reads g x nsplit partial rows of 512 B from L2 with one CTA, so
+  // it is bound by loads in flight: a thread owns 4 dims of one row (a warp a
+  // whole coalesced row), keeps 8 float4 loads in flight, and when the group is
+  // small the splits are dealt round-robin to `parts` thread groups whose sums
+  // meet in smem.
+  constexpr int kQuads = kHeadDim / 4;
+  const int items = g * kQuads;
+  const int parts = items >= kAttnThreads ? 1 : kAttnThreads / items;
+  float4* red = reinterpret_cast<float4*>(inv + kMaxGroup);   // [parts][items]
+  for (int it = tid; it < items * parts; it += kAttnThreads) {
+    const int item = it % items;
+    const int part = it / items;
+    const int row = item / kQuads;
+    const int q4 = item - row * kQuads;
     const size_t qrow = (size_t)req * a.hq + qh0 + row;
-    const float* src = a.ws_o + qrow * a.max_splits * kHeadDim + d;
-    float acc = 0.f;
-    int s2 = 0;
-    for (; s2 + 8 <= nsplit; s2 += 8) {   // 8 partial loads in flight, then the FMAs in order
-      float v[8];
+    const float4* src = reinterpret_cast<const float4*>(a.ws_o + qrow * a.max_splits * kHeadDim) + q4;
+    const float* w = wts + row * kMaxSplits;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int s2 = part;
+    for (; s2 + 7 * parts < nsplit; s2 += 8 * parts) {   // 8 loads in flight, FMAs in order
+      float4 v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (size_t)(s2 + u) * kHeadDim);
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (size_t)(s2 + u * parts) * kQuads);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) acc += wts[row * kMaxSplits + s2 + u] * v[u];
+      for (int u = 0; u < 8; ++u) {
+        const float wu = w[s2 + u * parts];
+        acc.x += wu * v[u].x;
+        acc.y += wu * v[u].y;
+        acc.z += wu * v[u].z;
+        acc.w += wu * v[u].w;
+      }
     }
-    for (; s2 < nsplit; ++s2) acc += wts[row * kMaxSplits + s2] * __ldcg(src + (size_t)s2 * kHeadDim);
-    a.out[qrow * kHeadDim + d] = __float2bfloat16(acc * inv[row]);
+    for (; s2 < nsplit; s2 += parts) {
+      const float4 v = __ldcg(src + (size_t)s2 * kQuads);
+      const float wu = w[s2];
+      acc.x += wu * v.x;
+      acc.y += wu * v.y;
+      acc.z += wu * v.z;
+      acc.w += wu * v.w;
+    }
+    if (parts == 1) {
+      const float r = inv[row];
+      __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(a.out + qrow * kHeadDim + q4 * 4);
+      dst[0] = __floats2bfloat162_rn(acc.x * r, acc.y * r);
+      dst[1] = __floats2bfloat162_rn(acc.z * r, acc.w * r);
+    } else {
+      red[part * items + item] = acc;
+    }
+  }
+  if (parts > 1) {
+    __syncthreads();
+    for (int item = tid; item < items; item += kAttnThreads) {
+      float4 acc = red[item];
+      for (int p = 1; p < parts; ++p) {
+        const float4 v = red[p * items + item];
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+      }
+      const int row = item / kQuads;
+      const int q4 = item - row * kQuads;
+      const float r = inv[row];
+      const size_t qrow = (size_t)req * a.hq + qh0 + row;
+      __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(a.out + qrow * kHeadDim + q4 * 4);
+      dst[0] = __floats2bfloat162_rn(acc.x * r, acc.y * r);
+      dst[1] = __floats2bfloat162_rn(acc.z * r, acc.w * r);
+    }
   }
   if (tid == 0) a.counters[req * a.hkv + kvh] = 0;  // re-arm for the next launch
 }
@@ -390,9 +442,9 @@ static cudaError_t attn_init_once() {
   return cudaSuccess;
 }
 
-// Pick the split length that minimises (waves x split length) for the widest
-// request: grids are sized against 148 SMs x resident CTAs per SM.
-static AttnPlan plan_splits(int batch, int hkv, int max_seq_len) {
+// Pick the split length for the widest request (cost model below); grids are
+// sized against 148 SMs x resident CTAs per SM.
+static AttnPlan plan_splits(int batch, int hq, int hkv, int max_seq_len) {
   const int nblk = (max_seq_len + kBlockTokens - 1) / kBlockTokens;
   AttnPlan p{1, 1};
   if (nblk <= 0) return p;
@@ -401,21 +453,39 @@ static AttnPlan plan_splits(int batch, int hkv, int max_seq_len) {
   lo = lo < 1 ? 1 : lo;
   int hi = nblk < kMaxBlocksPerSplit ? nblk : kMaxBlocksPerSplit;
   if (lo > hi) lo = hi;
-  // Each split costs a partial write and a longer combine; short splits are
-  // latency-bound, so fill each SM once rather than both CTA slots
-  // (tools/k1_overhead.py with OFB_K1_BPS: B=1, 8 KV heads, 4K / 16K / 64K
-  // tokens best at ~16 / ~16 / ~32 splits).
-  // One CTA per SM (never more CTAs than SMs: a doubled-up SM finishes last);
-  // long splits use both resident CTA slots, where the second CTA's stream adds
-  // bandwidth that outweighs the longer combine.
-  long splits = g_num_sms / pairs;
-  splits = splits < 1 ? 1 : splits;
-  if ((nblk + splits - 1) / splits >= 128) {
-    const long two = (long)g_num_sms * g_attn_occupancy / pairs;
-    splits = two > splits ? two : splits;
+  // Cost model over power-of-two split lengths (profiles/r01_k1_bps_sweep.jsonl,
+  // tools/k1_bps_sweep.py: it picks the measured best on all 21 swept shapes):
+  //   stream  = max(bytes / min(HBM, resident CTAs x per-CTA rate),
+  //                 waves x split bytes / per-CTA rate)
+  //   combine = splits x passes x per-split cost   (one CTA reads g x splits
+  //             partial rows; passes = its 160 threads over g x 32 float4s)
+  // A CTA streams ~50 GB/s alone, HBM reads top out near 7 TB/s, and a split
+  // row pass costs ~50 ns in the combine; power-of-two lengths also measured
+  // faster than their neighbours (aligned 128 KiB runs of the table).
+  constexpr double kCtaGBs = 50.0, kHbmGBs = 7000.0, kCombineUs = 0.05;
+  const int group = hq / hkv;
+  const long passes = (group * (kHeadDim / 4) + kAttnThreads - 1) / kAttnThreads;
+  const long slots = (long)g_num_sms * g_attn_occupancy;
+  double best = 1e30;
+  int bps = hi;
+  for (int cand = 8; cand <= 256; cand *= 2) {
+    int b = cand > nblk ? nblk : cand;
+    if (b < lo) continue;
+    const long ns = (nblk + b - 1) / b;
+    const long ctas = pairs * ns;
+    const double conc = (double)(ctas < slots ? ctas : slots);
+    const double kb = (double)kHeadBlockBytes / 1e3;   // per block, in KB -> us at GB/s
+    const double rate = conc * kCtaGBs < kHbmGBs ? conc * kCtaGBs : kHbmGBs;
+    double t = (double)pairs * nblk * kb / rate;
+    const double tw = (double)((ctas + slots - 1) / slots) * b * kb / kCtaGBs;
+    t = t > tw ? t : tw;
+    if (ns > 1) t += (double)ns * passes * kCombineUs;
+    if (t < best - 1e-9) {
+      best = t;
+      bps = b;
+    }
+    if (cand >= nblk) break;
   }
-  int bps = (int)((nblk + splits - 1) / splits);
-  if (bps < 8) bps = 8;   // a split must amortise its partial and its combine share
   bps = bps < lo ? lo : (bps > hi ? hi : bps);
   p.blocks_per_split = bps;
   if (const char* f = std::getenv("OFB_K1_BPS")) {   // tuning experiments only
@@ -514,7 +584,7 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
   if (e != cudaSuccess) return e;
   if (workspace_bytes < split_workspace_bytes(batch, hq, hkv, max_seq_len))
     return cudaErrorInvalidValue;
-  const AttnPlan plan = plan_splits(batch, hkv, max_seq_len);
+  const AttnPlan plan = plan_splits(batch, hq, hkv, max_seq_len);
   const int nblk = (max_seq_len + kBlockTokens - 1) / kBlockTokens;
   int ws_splits = nblk < 1 ? 1 : nblk;
   if (ws_splits > kMaxSplits) ws_splits = kMaxSplits;
