@@ -20,6 +20,7 @@ step.  ``roofline``: K1 (the dominant kernel) vs measured HBM copy peak;
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -492,11 +493,21 @@ def run_ours(args, cfg):
         step(i, e2e=True)
     clean_boundary()
     pf0 = ex.runtime.prefetch_stats()
+    gc_pauses = []          # interpreter GC pauses inside the e2e region (host outliers)
+    gc_t0 = [0.0]
+
+    def _gc_cb(phase, info):
+        if phase == "start":
+            gc_t0[0] = time.perf_counter()
+        else:
+            gc_pauses.append((info.get("generation"), round((time.perf_counter() - gc_t0[0]) * 1e3, 3)))
+    gc.callbacks.append(_gc_cb)
     e0 = time.perf_counter()
     e2e_steps = max(8, args.steps)
     marks = [e0]
     run_steps(e2e_steps, e2e=True, marks=marks)
     barrier()
+    gc.callbacks.remove(_gc_cb)
     e2e_step_ms = [(b - a) * 1e3 for a, b in zip(marks, marks[1:])]
     pf1 = ex.runtime.prefetch_stats()
     e2e_ms = (time.perf_counter() - e0) * 1e3 / e2e_steps
@@ -569,6 +580,7 @@ def run_ours(args, cfg):
         "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": h2d_in, "d2h_bytes_per_step": d2h_out,
                 "step_ms": [round(x, 3) for x in e2e_step_ms],
+                "gc_pauses": [{"gen": g_, "ms": m_} for g_, m_ in gc_pauses if m_ >= 0.5],
                 "prefetch_adopted_steps": pf1["adopted"] - pf0["adopted"],
                 "prefetch_dropped_steps": pf1["dropped"] - pf0["dropped"]},
         "roofline": {"bound": "hbm", "kernel": ("K1 paged GQA decode (" + ("paged_gqa_decode_kernel, split variant"

@@ -300,6 +300,8 @@ typedef struct ofb_plan_result {
   int32_t status;         /* 0 plan, 1 no placement fits the budget, 2 cap unsatisfiable */
   int32_t decode_window, expiry_step;
   int64_t candidates_feasible, candidates_priced, candidates_ranked;
+  int32_t enumeration_windows;   /* device_enumerate: sorted windows materialised (bounded
+                                    memory: the list is served in runs of whole keys) */
 } ofb_plan_result;
 
 OFB_API int ofb_plan_solve(const ofb_plan_problem* problem, ofb_plan_result* result);

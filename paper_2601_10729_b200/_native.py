@@ -77,7 +77,7 @@ class PlanResult(ctypes.Structure):
 
     _fields_ = [("status", c_i32), ("decode_window", c_i32), ("expiry_step", c_i32),
                 ("candidates_feasible", c_i64), ("candidates_priced", c_i64),
-                ("candidates_ranked", c_i64)]
+                ("candidates_ranked", c_i64), ("enumeration_windows", c_i32)]
 
 
 class OprojDesc(ctypes.Structure):

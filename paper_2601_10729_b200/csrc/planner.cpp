@@ -27,6 +27,7 @@
 #include <queue>
 #include <stdexcept>
 #include <string>
+#include <cstdlib>
 #include <thread>
 #include <vector>
 
@@ -38,6 +39,7 @@ int plan_gpu_enumerate(int B, int C, int L, const int* count, const uint8_t* mas
                        void** handle, int64_t* n_feasible, std::string* err);
 int plan_gpu_fetch(void* handle, int64_t from, int64_t count, uint64_t* dst, std::string* err);
 void plan_gpu_free(void* handle);
+int plan_gpu_windows(void* handle);
 }  // namespace ofb
 
 namespace {
@@ -543,7 +545,7 @@ struct Ranker {
     const double compL = P.comp * (double)op.L, bw = P.p->bandwidth_blocks_per_ms;
     int pick[64];
     for (uint64_t k : keys) {
-      const int64_t idx = (int64_t)(k & 0xffffffffull);
+      const int64_t idx = (int64_t)k;   // plan_gpu_fetch returns enumeration indices
       decode(idx, op.C, B, pick);
       int64_t fetch = 0;
       for (int r = 0; r < B; ++r) fetch += P.p->blocks[r] * op.count[pick[r]];
@@ -690,7 +692,14 @@ int ofb_plan_solve(const ofb_plan_problem* p, ofb_plan_result* out) {
   Problem P(p);
   int64_t space = 1;
   for (int r = 0; r < p->batch; ++r) space *= P.op.C;
-  if (space > (int64_t)1 << 28) {
+  // host DFS: 2^28 (its list lives in host memory); GPU enumeration: 2^36,
+  // served in bounded windows
+  int host_log2 = 28;
+  if (const char* v = std::getenv("OFB_PLAN_HOST_SPACE_LOG2")) {   // tests: oracle runs past 2^28
+    const int x = std::atoi(v);
+    if (x > 0 && x <= 36) host_log2 = x;
+  }
+  if (space > ((int64_t)1 << (p->device_enumerate ? 36 : host_log2))) {
     g_plan_err = "candidate space too large for exhaustive search";
     return -1;
   }
@@ -704,12 +713,15 @@ int ofb_plan_solve(const ofb_plan_problem* p, ofb_plan_result* out) {
     return -1;
   }
   if (!any) {
+    out->enumeration_windows = rk.gpu ? ofb::plan_gpu_windows(rk.gpu) : 0;
     out->status = 1;  // no placement fits the GPU block budget
     return 0;
   }
   out->candidates_feasible = rk.total;
   try {
-    return solve_ranked(p, P, rk, out);
+    const int rc = solve_ranked(p, P, rk, out);
+    out->enumeration_windows = rk.gpu ? ofb::plan_gpu_windows(rk.gpu) : 0;
+    return rc;
   } catch (const std::exception& e) {   // a GPU chunk pull failed
     g_plan_err = e.what();
     return -1;

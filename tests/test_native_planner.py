@@ -140,3 +140,87 @@ def test_gpu_enumeration_b8_l32():
         planner.SOLVER = old
     assert a == b
     assert t_gpu < t_host, (t_gpu, t_host)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("window,shapes", [(5, ((4, 4), (9, 3))),
+                                           (300, ((4, 4), (9, 3), (12, 4), (32, 4), (32, 5))),
+                                           (5000, ((4, 4), (9, 3), (12, 4), (32, 4), (32, 5)))])
+def test_gpu_enumeration_windows_match_host(window, shapes, monkeypatch):
+    """The GPU candidate list is served in bounded windows (whole lower-bound
+    keys, or index ranges of one oversized key): forcing tiny windows changes
+    nothing in the plans, windows and latencies."""
+    monkeypatch.setenv("OFB_PLAN_WINDOW", str(window))
+    rng = random.Random(4242 + window)
+    multi = 0
+    for L, B in shapes:
+        for _ in range(4):
+            batch, prof, slo, paused, snap = _instance(rng, L, B)
+            for cap_only in (False, True):
+                def run():
+                    if cap_only:
+                        return _plan_sig(planner.solve_capacity_only(batch, prof, slo, 3))
+                    return _plan_sig(planner.solve(batch, prof, slo, 3, paused=paused,
+                                                   deposit_snapshot=snap))
+                old = planner.SOLVER
+                try:
+                    planner.SOLVER = "native"
+                    a = run()
+                    planner.SOLVER = "native-gpu"
+                    b = run()
+                    multi += (planner.LAST_NATIVE_STATS or {}).get("windows", 0) > 1
+                finally:
+                    planner.SOLVER = old
+                assert a == b
+    assert multi > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("L,B", [(4, 9), (4, 10)])
+def test_gpu_enumeration_past_b8_matches_numpy(L, B, monkeypatch):
+    """Batches past the host solver's range (B = 9-10) against the numpy
+    restatement, with small windows so several are materialised."""
+    monkeypatch.setenv("OFB_PLAN_WINDOW", "20000")
+    rng = random.Random(9000 + L * 10 + B)
+    for _ in range(2):
+        batch, prof, slo, paused, snap = _instance(rng, L, B)
+        old = planner.SOLVER
+        try:
+            planner.SOLVER = "native-gpu"
+            a = _plan_sig(planner.solve(batch, prof, slo, 2, paused=paused, deposit_snapshot=snap))
+            c = _plan_sig(planner.solve_capacity_only(batch, prof, slo, 2))
+            planner.SOLVER = "python"
+            b = _plan_sig(planner.solve(batch, prof, slo, 2, paused=paused, deposit_snapshot=snap))
+            d = _plan_sig(planner.solve_capacity_only(batch, prof, slo, 2))
+        finally:
+            planner.SOLVER = old
+        assert a == b
+        assert c == d
+
+
+@pytest.mark.gpu
+def test_gpu_enumeration_b9_l32_matches_host(monkeypatch):
+    """B = 9 at L = 32 (2.36 G candidates, past the 2^32 index of the previous
+    composite key): the windowed GPU enumeration equals the host DFS run past
+    its default range."""
+    from paper_2601_10729_b200 import defaults
+    from paper_2601_10729_b200.calibrate import b200_profile
+
+    monkeypatch.setenv("OFB_PLAN_HOST_SPACE_LOG2", "32")
+    monkeypatch.setattr(planner, "_NATIVE_MAX_SPACE", 1 << 32)
+    rng = random.Random(9)
+    prof = b200_profile(32, 8, gpu_block_budget=60000 * 9 // 4)
+    batch = [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=rng.randint(2000, 30000),
+                          target_output_tokens=64) for i in range(9)]
+    slo = defaults.default_slo(prof, 60.0)
+    old = planner.SOLVER
+    try:
+        planner.SOLVER = "native-gpu"
+        b = _plan_sig(planner.solve(batch, prof, slo, 1))
+        stats = dict(planner.LAST_NATIVE_STATS)
+        planner.SOLVER = "native"
+        a = _plan_sig(planner.solve(batch, prof, slo, 1))
+    finally:
+        planner.SOLVER = old
+    assert stats["feasible"] > 0
+    assert a == b

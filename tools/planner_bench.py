@@ -1,6 +1,13 @@
 """Exact-solve latency: reference kvsim (if importable) vs this package's numpy
-restatement vs the native solver, on a B200-calibrated 8B profile (L=32).
-Every plan is compared for bit-identity."""
+restatement vs the native solver (host DFS, GPU enumeration), on a
+B200-calibrated 8B profile (L=32).  Every plan is compared for bit-identity.
+
+    python tools/planner_bench.py [--max-batch 10] [--host-max 8]
+
+B = 9-10 (2.4 G / 26 G candidates) run on the GPU enumeration only, unless
+--host-max raises the host DFS's range (OFB_PLAN_HOST_SPACE_LOG2, needs memory).
+"""
+import argparse
 import json
 import random
 import sys
@@ -26,19 +33,32 @@ def sig(p):
             p.predicted_latency.total_latency_ms.hex())
 
 
+ap = argparse.ArgumentParser()
+ap.add_argument("--max-batch", type=int, default=8)
+ap.add_argument("--min-batch", type=int, default=1)
+ap.add_argument("--host-max", type=int, default=8)
+args = ap.parse_args()
+if args.host_max > 8:
+    import os
+
+    os.environ["OFB_PLAN_HOST_SPACE_LOG2"] = "36"
+    planner._NATIVE_MAX_SPACE = 1 << 36
+
 rows = []
-for B in range(1, 9):
+for B in range(args.min_batch, args.max_batch + 1):
     rng = random.Random(B)
     prof = b200_profile(32, 8, gpu_block_budget=60000 * B // 4)
     batch = [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=rng.randint(2000, 30000),
                           target_output_tokens=64) for i in range(B)]
     slo = defaults.default_slo(prof, 60.0)
     rec = {"batch": B}
-    planner.SOLVER = "native"
-    t = time.perf_counter(); p_nat = planner.solve(batch, prof, slo, 1)
-    rec["native_ms"] = (time.perf_counter() - t) * 1e3
-    rec["plan"] = sig(p_nat)[0] if sig(p_nat)[0] == "infeasible" else [r.count(0) for r in p_nat.placement.rows]
-    rec["native_stats"] = planner.LAST_NATIVE_STATS
+    p_nat = None
+    if B <= args.host_max:
+        planner.SOLVER = "native"
+        t = time.perf_counter(); p_nat = planner.solve(batch, prof, slo, 1)
+        rec["native_ms"] = (time.perf_counter() - t) * 1e3
+        rec["plan"] = sig(p_nat)[0] if sig(p_nat)[0] == "infeasible" else [r.count(0) for r in p_nat.placement.rows]
+        rec["native_stats"] = planner.LAST_NATIVE_STATS
     try:
         import torch
 
@@ -47,7 +67,12 @@ for B in range(1, 9):
             planner.solve(batch, prof, slo, 1)             # warm-up (context, cub)
             t = time.perf_counter(); p_gpu = planner.solve(batch, prof, slo, 1)
             rec["native_gpu_ms"] = (time.perf_counter() - t) * 1e3
-            rec["native_gpu_equal"] = sig(p_gpu) == sig(p_nat)
+            rec["native_gpu_stats"] = planner.LAST_NATIVE_STATS
+            if p_nat is not None:
+                rec["native_gpu_equal"] = sig(p_gpu) == sig(p_nat)
+            else:
+                rec["plan"] = (sig(p_gpu)[0] if sig(p_gpu)[0] == "infeasible"
+                               else [r.count(0) for r in p_gpu.placement.rows])
             planner.SOLVER = "native"
     except ImportError:
         pass
