@@ -52,6 +52,11 @@ def _run_oracle(case):
     ([3000, 5], 64, 8),                          # Llama-3.1-70B heads (group 8)
     ([777], 16, 1),                              # group 16 (max)
     ([513, 64], 4, 4),                           # MHA (group 1)
+    # long single requests: many splits, so the combine runs with 5 / 2 / 1
+    # thread groups dealing the splits (groups 1 / 2 / 16)
+    ([20000, 3], 2, 2),
+    ([24001], 4, 2),
+    ([30000, 700], 16, 1),
 ])
 def test_attention_matches_oracle(seq_lens, hq, hkv):
     case = make_case(seq_lens, hq, hkv, seed=sum(seq_lens) + hq)
