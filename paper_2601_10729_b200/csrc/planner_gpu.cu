@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -157,19 +158,24 @@ struct Handle {
 // engine re-plans every few steps; fresh cudaMalloc/cudaFree of the window
 // buffers cost more than a small solve).
 cudaMemPool_t plan_pool() {
-  static cudaMemPool_t pool = nullptr;
-  if (!pool) {
-    int dev = 0;
-    cudaGetDevice(&dev);
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pools[dev]) {
     cudaMemPoolProps props = {};
     props.allocType = cudaMemAllocationTypePinned;
     props.location.type = cudaMemLocationTypeDevice;
     props.location.id = dev;
-    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) return nullptr;
-    unsigned long long keep = 2ull << 30;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    if (cudaMemPoolCreate(&pools[dev], &props) != cudaSuccess) {
+      pools[dev] = nullptr;
+      return nullptr;
+    }
+    unsigned long long keep = 2ull << 30;   // keep up to one window's buffers cached
+    cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
   }
-  return pool;
+  return pools[dev];
 }
 
 template <typename T>
