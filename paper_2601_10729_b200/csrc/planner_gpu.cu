@@ -395,8 +395,11 @@ int plan_gpu_fetch(void* handle, int64_t from, int64_t count, uint64_t* dst, std
     while (from >= h->wstart + h->wn)
       if (!advance(h, err)) return -1;
     const int64_t take = std::min<int64_t>(count, h->wstart + h->wn - from);
-    cudaError_t e = cudaMemcpy(dst, h->sorted + (from - h->wstart), (size_t)take * 8,
-                               cudaMemcpyDeviceToHost);
+    // on the handle's non-blocking stream: a re-plan never waits for decode
+    // steps queued on the legacy default stream
+    cudaError_t e = cudaMemcpyAsync(dst, h->sorted + (from - h->wstart), (size_t)take * 8,
+                                    cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) {
       *err = std::string("plan_gpu_fetch: ") + cudaGetErrorString(e);
       return -1;

@@ -5,6 +5,7 @@ time per split x query head).
 
     python tools/k1_bps_sweep.py > k1_bps.jsonl
 """
+import argparse
 import json
 import os
 import statistics
@@ -18,9 +19,15 @@ from paper_2601_10729_b200 import ops  # noqa: E402
 
 dev = torch.device("cuda:0")
 ops.set_attention_kernel("split")
-SHAPES = [(1, 8, 1), (4, 8, 1), (16, 8, 1), (1, 32, 8), (4, 32, 8), (1, 64, 8), (1, 16, 1)]
-SEQS = [4096, 16384, 65536]
-BPS = [None, 2, 4, 8, 12, 16, 24, 32, 48, 64, 96, 128, 256]
+ap = argparse.ArgumentParser()
+ap.add_argument("--shapes", default="1,8,1;4,8,1;16,8,1;1,32,8;4,32,8;1,64,8;1,16,1",
+                help="batch,hq,hkv;...")
+ap.add_argument("--seqs", default="4096,16384,65536")
+ap.add_argument("--bps", default="2,4,8,12,16,24,32,48,64,96,128,256")
+args = ap.parse_args()
+SHAPES = [tuple(int(x) for x in t.split(",")) for t in args.shapes.split(";")]
+SEQS = [int(x) for x in args.seqs.split(",")]
+BPS = [None] + [int(x) for x in args.bps.split(",")]
 
 
 def time_launch(q, pools, bt, lens, out, seq, ws, iters=20):
