@@ -21,7 +21,33 @@ for variant in ("stream", "split"):
         ops.decode_attention(case["q"].to(dev), case["pool"].to(dev),
                              torch.from_numpy(case["block_tables"]).to(dev),
                              torch.from_numpy(case["seq_lens"]).to(dev), scale=1 / math.sqrt(128))
+# split combine with 5 / 2 / 1 thread groups dealing the splits (groups 1 / 2 / 16)
+ops.set_attention_kernel("split")
+for lens, hq, hkv in (([6000, 3], 2, 2), ([6001], 4, 2), ([8000, 70], 16, 1)):
+    case = make_case(lens, hq, hkv, seed=2)
+    ops.decode_attention(case["q"].to(dev), case["pool"].to(dev),
+                         torch.from_numpy(case["block_tables"]).to(dev),
+                         torch.from_numpy(case["seq_lens"]).to(dev), scale=1 / math.sqrt(128))
 ops.set_attention_kernel("auto")
+
+# planner GPU enumeration: histogram + windowed materialisation (tiny windows)
+import os  # noqa: E402
+import random  # noqa: E402
+
+from paper_2601_10729_b200 import planner  # noqa: E402
+from paper_2601_10729_b200.calibrate import b200_profile  # noqa: E402
+from paper_2601_10729_b200 import defaults  # noqa: E402
+
+os.environ["OFB_PLAN_WINDOW"] = "50"
+rng = random.Random(3)
+prof = b200_profile(8, 8, gpu_block_budget=400)
+preqs = [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=rng.randint(200, 900),
+                      target_output_tokens=16) for i in range(4)]
+planner.SOLVER = "native-gpu"
+planner.solve_capacity_only(preqs, prof, defaults.default_slo(prof, 60.0), 1)
+planner.SOLVER = "native"
+del os.environ["OFB_PLAN_WINDOW"]
+
 shape = ModelShape(4, 8, 2)
 batch = [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=200 + 70 * i, target_output_tokens=8)
          for i in range(3)]
