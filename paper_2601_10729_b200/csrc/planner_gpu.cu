@@ -342,7 +342,7 @@ int plan_gpu_enumerate(int B, int C, int L, const int* count, const uint8_t* mas
   }
   if (const char* w = std::getenv("OFB_PLAN_WINDOW")) {   // tests: force small windows
     const long long v = std::atoll(w);
-    if (v > 0) h->window_cap = v;
+    if (v > 0 && v <= (1ll << 30)) h->window_cap = v;
   }
   const size_t nbins = (size_t)max_fetch + 2;
   unsigned long long* d_hist = nullptr;
