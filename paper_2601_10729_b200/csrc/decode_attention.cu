@@ -80,6 +80,20 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
   const bool early = a.kv_ready != 0;
   if (!early) pdl_wait();
   pdl_trigger();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kRingBytes);
+  uint64_t* empty = full + kStages;
+  int32_t* blk_ids = reinterpret_cast<int32_t*>(empty + kStages);
+  int* flag = blk_ids + kMaxBlocksPerSplit;
+  // The split's table run is loaded speculatively (bounded by the row, not by
+  // the sequence length) so it does not wait for the seq_lens round trip.
+  const int b_begin = split * a.blocks_per_split;
+  {
+    const int span = min(a.blocks_per_split, a.max_blocks - b_begin);
+    const int32_t* bt = a.block_tables + (size_t)req * a.max_blocks + b_begin;
+    for (int i = tid; i < span; i += kAttnThreads) blk_ids[i] = bt[i];
+  }
   const int seq = a.seq_lens[req];
   const int nblk = (seq + kBlockTokens - 1) / kBlockTokens;
   const int nsplit = (nblk + a.blocks_per_split - 1) / a.blocks_per_split;
@@ -95,18 +109,8 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
     return;
   }
   if (split >= nsplit) return;
-  const int b_begin = split * a.blocks_per_split;
   const int n = min(a.blocks_per_split, nblk - b_begin);
 
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kRingBytes);
-  uint64_t* empty = full + kStages;
-  int32_t* blk_ids = reinterpret_cast<int32_t*>(empty + kStages);
-  int* flag = blk_ids + kMaxBlocksPerSplit;
-
-  const int32_t* bt = a.block_tables + (size_t)req * a.max_blocks + b_begin;
-  for (int i = tid; i < n; i += kAttnThreads) blk_ids[i] = bt[i];
   if (tid == 0) {
     prefetch_tma_desc(&kv_map);
     for (int s = 0; s < kStages; ++s) {
