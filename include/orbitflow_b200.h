@@ -46,6 +46,13 @@ OFB_API const char* ofb_last_error(void);
 OFB_API int ofb_set_attention_kernel(int32_t variant);
 /* Which decomposition a launch of this shape would use now: 0 stream-K, 1 split. */
 OFB_API int ofb_attention_variant_for(int32_t batch, int32_t num_kv_heads, int32_t max_seq_len);
+/* Split plan of the (default) split K1, host arithmetic only: blocks per split
+ * and splits per (request, KV head) on a GPU with `num_sms` SMs and
+ * `ctas_per_sm` resident K1 CTAs (ofb_device_info); the launch uses the same
+ * function with the live device's values. */
+OFB_API int ofb_attention_split_plan(int32_t batch, int32_t num_q_heads, int32_t num_kv_heads,
+                                     int32_t max_seq_len, int32_t num_sms, int32_t ctas_per_sm,
+                                     int32_t* blocks_per_split, int32_t* splits);
 /* Diagnostics: stream-K K1 launches write 6 globaltimer stamps per CTA (entry,
  * past the dependency wait, first tile ready, last tile consumed, exit, SM id)
  * into `device_buffer` (uint64 [448][6]); NULL switches tracing off. */

@@ -100,6 +100,8 @@ SIGNATURES = {
     "ofb_set_attention_kernel": (ctypes.c_int, [c_i32]),
     "ofb_k1_trace": (ctypes.c_int, [c_vp]),
     "ofb_attention_variant_for": (ctypes.c_int, [c_i32, c_i32, c_i32]),
+    "ofb_attention_split_plan": (ctypes.c_int, [c_i32, c_i32, c_i32, c_i32, c_i32, c_i32,
+                                                ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)]),
     "ofb_device_info": (ctypes.c_int, [c_i32p, c_i32p]),
     "ofb_host_alloc": (c_vp, [c_i64]),
     "ofb_host_free": (ctypes.c_int, [c_vp]),

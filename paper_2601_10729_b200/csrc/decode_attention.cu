@@ -448,7 +448,7 @@ static cudaError_t attn_init_once() {
 
 // Pick the split length for the widest request (cost model below); grids are
 // sized against 148 SMs x resident CTAs per SM.
-static AttnPlan plan_splits(int batch, int hq, int hkv, int max_seq_len) {
+static AttnPlan plan_splits(int batch, int hq, int hkv, int max_seq_len, int num_sms, int occupancy) {
   const int nblk = (max_seq_len + kBlockTokens - 1) / kBlockTokens;
   AttnPlan p{1, 1};
   if (nblk <= 0) return p;
@@ -469,7 +469,7 @@ static AttnPlan plan_splits(int batch, int hq, int hkv, int max_seq_len) {
   constexpr double kCtaGBs = 50.0, kHbmGBs = 7000.0, kCombineUs = 0.05;
   const int group = hq / hkv;
   const long passes = (group * (kHeadDim / 4) + kAttnThreads - 1) / kAttnThreads;
-  const long slots = (long)g_num_sms * g_attn_occupancy;
+  const long slots = (long)num_sms * occupancy;
   double best = 1e30;
   int bps = hi;
   for (int cand = 8; cand <= 256; cand *= 2) {
@@ -543,6 +543,19 @@ bool pdl_enabled() {
   return on == 1;
 }
 
+// Host arithmetic only (no device): the split plan a launch would use on a GPU
+// with `num_sms` SMs and `occupancy` resident K1 CTAs per SM.
+int attention_split_plan(int batch, int hq, int hkv, int max_seq_len, int num_sms, int occupancy,
+                         int* blocks_per_split, int* splits) {
+  if (batch < 1 || hkv < 1 || hq % hkv != 0 || hq / hkv > kMaxGroup || max_seq_len < 0 ||
+      num_sms < 1 || occupancy < 1 || !blocks_per_split || !splits)
+    return -1;
+  const AttnPlan p = plan_splits(batch, hq, hkv, max_seq_len, num_sms, occupancy);
+  *blocks_per_split = p.blocks_per_split;
+  *splits = p.max_splits;
+  return 0;
+}
+
 int attention_variant_for(int batch, int hkv, int max_seq_len) {
   return use_split_kernel(batch, hkv, max_seq_len) ? 1 : 0;
 }
@@ -588,7 +601,7 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
   if (e != cudaSuccess) return e;
   if (workspace_bytes < split_workspace_bytes(batch, hq, hkv, max_seq_len))
     return cudaErrorInvalidValue;
-  const AttnPlan plan = plan_splits(batch, hq, hkv, max_seq_len);
+  const AttnPlan plan = plan_splits(batch, hq, hkv, max_seq_len, g_num_sms, g_attn_occupancy);
   const int nblk = (max_seq_len + kBlockTokens - 1) / kBlockTokens;
   int ws_splits = nblk < 1 ? 1 : nblk;
   if (ws_splits > kMaxSplits) ws_splits = kMaxSplits;

@@ -36,6 +36,8 @@ cudaError_t launch_kv_append(const void* k_new, const void* v_new, void* pool,
 int attention_occupancy();
 int set_attention_variant(int variant);
 int attention_variant_for(int batch, int hkv, int max_seq_len);
+int attention_split_plan(int batch, int hq, int hkv, int max_seq_len, int num_sms, int occupancy,
+                         int* blocks_per_split, int* splits);
 void set_k1_trace_buffer(void* buf);
 cudaError_t launch_kv_prefill(const void* k, const void* v, const uint64_t* dst, int num_layers,
                               int tokens, int hkv, cudaStream_t stream);
@@ -346,6 +348,15 @@ int ofb_set_attention_kernel(int32_t variant) {
 
 int ofb_attention_variant_for(int32_t batch, int32_t num_kv_heads, int32_t max_seq_len) {
   return ofb::attention_variant_for(batch, num_kv_heads, max_seq_len);
+}
+
+int ofb_attention_split_plan(int32_t batch, int32_t num_q_heads, int32_t num_kv_heads,
+                             int32_t max_seq_len, int32_t num_sms, int32_t ctas_per_sm,
+                             int32_t* blocks_per_split, int32_t* splits) {
+  if (ofb::attention_split_plan(batch, num_q_heads, num_kv_heads, max_seq_len, num_sms, ctas_per_sm,
+                                blocks_per_split, splits) != 0)
+    return ofb::report_error(-1, "ofb_attention_split_plan: bad arguments");
+  return 0;
 }
 
 int ofb_k1_trace(void* device_buffer) {

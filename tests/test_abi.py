@@ -103,3 +103,55 @@ def test_runtime_calls_without_a_runtime_fail_cleanly():
     assert lib.ofb_runtime_prefetch_fence(None, None) == -1
     assert "null runtime" in lib.ofb_last_error().decode()
     assert lib.ofb_runtime_step_layers(None, 1) == -1
+
+
+# (batch, hq, hkv, context) -> split length measured fastest by tools/k1_bps_sweep.py
+# on the B200 box (profiles/r01_k1_bps_sweep.jsonl, 8..256 swept)
+_K1_BEST_BPS = {
+    (1, 8, 1, 4096): 16, (1, 8, 1, 16384): 32, (1, 8, 1, 65536): 64,
+    (4, 8, 1, 4096): 16, (4, 8, 1, 16384): 32, (4, 8, 1, 65536): 128,
+    (16, 8, 1, 4096): 32, (16, 8, 1, 16384): 64, (16, 8, 1, 65536): 256,
+    (1, 32, 8, 4096): 16, (1, 32, 8, 16384): 32, (1, 32, 8, 65536): 128,
+    (4, 32, 8, 4096): 32, (4, 32, 8, 16384): 128, (4, 32, 8, 65536): 256,
+    (1, 64, 8, 4096): 16, (1, 64, 8, 16384): 64, (1, 64, 8, 65536): 128,
+    (1, 16, 1, 4096): 16, (1, 16, 1, 16384): 32, (1, 16, 1, 65536): 64,
+}
+
+
+def _split_plan(lib, b, hq, hkv, seq, sms=148, occ=2):
+    import ctypes
+
+    bps, ns = ctypes.c_int32(), ctypes.c_int32()
+    assert lib.ofb_attention_split_plan(b, hq, hkv, seq, sms, occ, ctypes.byref(bps), ctypes.byref(ns)) == 0
+    return bps.value, ns.value
+
+
+def test_k1_split_plan_matches_measured_best():
+    """The split K1's cost model (host arithmetic, no GPU) picks the split length
+    the B200 sweep measured fastest on every swept latency-bound shape."""
+    from paper_2601_10729_b200 import _native
+
+    lib = _native.load()
+    for (b, hq, hkv, seq), best in _K1_BEST_BPS.items():
+        assert _split_plan(lib, b, hq, hkv, seq)[0] == best, (b, hq, hkv, seq)
+
+
+def test_k1_split_plan_invariants():
+    """Every plan covers the context within the kernel's limits (<= 256 splits of
+    <= 256 blocks), and a large step shape keeps the longest splits."""
+    import ctypes
+
+    from paper_2601_10729_b200 import _native
+
+    lib = _native.load()
+    for b in (1, 3, 16, 64):
+        for hq, hkv in ((8, 1), (32, 8), (64, 8), (16, 1), (4, 4)):
+            for seq in (0, 1, 15, 16, 17, 1000, 32768, 131072, 1 << 20):
+                bps, ns = _split_plan(lib, b, hq, hkv, seq)
+                nblk = -(-seq // 16)
+                assert 1 <= bps <= 256 and 1 <= ns <= 256
+                assert bps * ns >= nblk
+                assert ns == max(1, -(-nblk // bps))
+    assert _split_plan(lib, 16, 32, 8, 32768) == (256, 8)    # the cfg2 layer: 1024 CTAs
+    bad = ctypes.c_int32()
+    assert lib.ofb_attention_split_plan(1, 6, 4, 100, 148, 2, ctypes.byref(bad), ctypes.byref(bad)) != 0
