@@ -44,6 +44,7 @@ struct EnumArgs {
   double compL, bw;
   unsigned long long idx_begin, idx_end;   // enumeration range of this pass
   long long key_lo, key_hi;                // materialise pass: keep keys in [key_lo, key_hi]
+  unsigned long long out_cap;              // materialise pass: output capacity (overflow is counted, not written)
   int count[kMaxC];
   long long blocks[kMaxB];
 };
@@ -124,9 +125,8 @@ __global__ void materialise_kernel(const __grid_constant__ EnumArgs a, const uin
       unsigned long long slot = 0;
       if (lane == 0) slot = atomicAdd(n_out, (unsigned long long)__popc(ballot));
       slot = __shfl_sync(0xffffffffu, slot, 0);
-      if (keep)
-        out[slot + __popc(ballot & ((1u << lane) - 1u))] =
-            ((unsigned long long)key << a.idx_bits) | idx;
+      const unsigned long long at = slot + __popc(ballot & ((1u << lane) - 1u));
+      if (keep && at < a.out_cap) out[at] = ((unsigned long long)key << a.idx_bits) | idx;
     }
   }
 }
@@ -226,6 +226,7 @@ bool advance(Handle* h, std::string* err) {
     a.idx_end = h->total;
     h->next_key = k;
   }
+  a.out_cap = (unsigned long long)h->window_cap;
   unsigned long long got = 0;
   unsigned long long* d_n = nullptr;
   cudaStream_t s = h->stream;
