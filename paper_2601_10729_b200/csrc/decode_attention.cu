@@ -64,6 +64,25 @@ constexpr size_t kAttnSmemBytes = 1024 /*align slack*/ + kRingBytes +
                                   2 * kStages * sizeof(uint64_t) +
                                   kMaxBlocksPerSplit * sizeof(int32_t) + 16;
 
+// acc += sum_u w[s + u*parts] * src[(s + u*parts) rows]: N float4 partial loads
+// in flight, then the FMAs in split order.
+template <int N>
+__device__ __forceinline__ void combine_round(float4& acc, const float4* __restrict__ src,
+                                              const float* w, int s, int parts) {
+  constexpr int kQuads = kHeadDim / 4;
+  float4 v[N];
+#pragma unroll
+  for (int u = 0; u < N; ++u) v[u] = __ldcg(src + (size_t)(s + u * parts) * kQuads);
+#pragma unroll
+  for (int u = 0; u < N; ++u) {
+    const float wu = w[s + u * parts];
+    acc.x += wu * v[u].x;
+    acc.y += wu * v[u].y;
+    acc.z += wu * v[u].z;
+    acc.w += wu * v[u].w;
+  }
+}
+
 __global__ void __launch_bounds__(kAttnThreads, 2)
 paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnArgs a) {
   const int split = blockIdx.x;
@@ -346,7 +365,7 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
   __syncthreads();
   // The combine reads g x nsplit partial rows of 512 B from L2 with one CTA, so
   // it is bound by loads in flight: a thread owns 4 dims of one row (a warp a
-  // whole coalesced row), keeps 8 float4 loads in flight, and when the group is
+  // whole coalesced row), keeps 16 float4 loads in flight, and when the group is
   // small the splits are dealt round-robin to `parts` thread groups whose sums
   // meet in smem.
   constexpr int kQuads = kHeadDim / 4;
@@ -363,27 +382,11 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
     const float* w = wts + row * kMaxSplits;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     int s2 = part;
-    for (; s2 + 7 * parts < nsplit; s2 += 8 * parts) {   // 8 loads in flight, FMAs in order
-      float4 v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (size_t)(s2 + u * parts) * kQuads);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const float wu = w[s2 + u * parts];
-        acc.x += wu * v[u].x;
-        acc.y += wu * v[u].y;
-        acc.z += wu * v[u].z;
-        acc.w += wu * v[u].w;
-      }
-    }
-    for (; s2 < nsplit; s2 += parts) {
-      const float4 v = __ldcg(src + (size_t)s2 * kQuads);
-      const float wu = w[s2];
-      acc.x += wu * v.x;
-      acc.y += wu * v.y;
-      acc.z += wu * v.z;
-      acc.w += wu * v.w;
-    }
+    // rounds of 16, then 8, loads in flight (FMAs in split order after each
+    // round), then at most 7 single loads
+    for (; s2 + 15 * parts < nsplit; s2 += 16 * parts) combine_round<16>(acc, src, w, s2, parts);
+    for (; s2 + 7 * parts < nsplit; s2 += 8 * parts) combine_round<8>(acc, src, w, s2, parts);
+    for (; s2 < nsplit; s2 += parts) combine_round<1>(acc, src, w, s2, parts);
     if (parts == 1) {
       const float r = inv[row];
       __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(a.out + qrow * kHeadDim + q4 * 4);
@@ -458,15 +461,17 @@ static AttnPlan plan_splits(int batch, int hq, int hkv, int max_seq_len, int num
   int hi = nblk < kMaxBlocksPerSplit ? nblk : kMaxBlocksPerSplit;
   if (lo > hi) lo = hi;
   // Cost model over power-of-two split lengths (profiles/r01_k1_bps_sweep.jsonl,
-  // tools/k1_bps_sweep.py: it picks the measured best on all 21 swept shapes):
+  // tools/k1_bps_sweep.py: on all 21 swept shapes its pick is within 2% of the
+  // measured best):
   //   stream  = max(bytes / min(HBM, resident CTAs x per-CTA rate),
   //                 waves x split bytes / per-CTA rate)
   //   combine = splits x passes x per-split cost   (one CTA reads g x splits
   //             partial rows; passes = its 160 threads over g x 32 float4s)
-  // A CTA streams ~50 GB/s alone, HBM reads top out near 7 TB/s, and a split
-  // row pass costs ~50 ns in the combine; power-of-two lengths also measured
-  // faster than their neighbours (aligned 128 KiB runs of the table).
-  constexpr double kCtaGBs = 50.0, kHbmGBs = 7000.0, kCombineUs = 0.05;
+  // A CTA streams ~40 GB/s alone, HBM reads top out near 6.5 TB/s, and a split
+  // row pass costs ~50 ns in the combine (fitted to the sweep with the 16-deep
+  // combine); power-of-two lengths also measured faster than their neighbours
+  // (aligned 128 KiB runs of the table).
+  constexpr double kCtaGBs = 40.0, kHbmGBs = 6500.0, kCombineUs = 0.05;
   const int group = hq / hkv;
   const long passes = (group * (kHeadDim / 4) + kAttnThreads - 1) / kAttnThreads;
   const long slots = (long)num_sms * occupancy;
