@@ -149,6 +149,11 @@ typedef struct ofb_step_desc {
    * around.  The next step adopts them if its transfer plan matches (and
    * counts them in its timing record), else they are fenced and re-issued. */
   const int64_t* next_fetch_bytes;
+  /* 0: one append of every resident row at step start (the token's K/V of all
+   * layers is known up front).  1: the append of layer l runs right before its
+   * attention, inside ofb_runtime_step_layers - a decoder whose k_new/v_new of
+   * layer l are produced by work the caller interleaves after layer l-1. */
+  int32_t append_per_layer;
 } ofb_step_desc;
 
 typedef struct ofb_step_timing {
@@ -193,6 +198,10 @@ OFB_API int ofb_runtime_decode_step(ofb_runtime* rt, const ofb_step_desc* desc, 
 OFB_API int ofb_runtime_step_begin(ofb_runtime* rt, const ofb_step_desc* desc, void* stream);
 OFB_API int ofb_runtime_step_layers(ofb_runtime* rt, int32_t count);
 OFB_API int ofb_runtime_step_end(ofb_runtime* rt);
+/* Abandon a step begun with ofb_runtime_step_begin after a caller-side failure:
+ * waits for the work already enqueued, drops any cross-step prefetch and leaves
+ * the runtime ready for the next step.  Never fails on an idle runtime. */
+OFB_API int ofb_runtime_step_abort(ofb_runtime* rt);
 /* Make `stream` wait for every cross-step prefetch still in flight and drop
  * it (call before reusing staging or host slabs, e.g. after a plan change or a
  * released request). */

@@ -40,6 +40,7 @@ class StepDesc(ctypes.Structure):
         ("host_slabs", c_vp), ("staging_dst", c_vp), ("fetch_bytes", c_vp),
         ("staging_slots", c_i32), ("record_timing", c_i32),
         ("next_fetch_bytes", c_vp),
+        ("append_per_layer", c_i32),
     ]
 
 
@@ -117,6 +118,7 @@ SIGNATURES = {
     "ofb_runtime_step_begin": (ctypes.c_int, [c_vp, ctypes.POINTER(StepDesc), c_vp]),
     "ofb_runtime_step_layers": (ctypes.c_int, [c_vp, c_i32]),
     "ofb_runtime_step_end": (ctypes.c_int, [c_vp]),
+    "ofb_runtime_step_abort": (ctypes.c_int, [c_vp]),
     "ofb_runtime_prefetch_fence": (ctypes.c_int, [c_vp, c_vp]),
     "ofb_runtime_prefetch_stats": (ctypes.c_int, [c_vp, c_i64p, c_i64p]),
     "ofb_runtime_migrate": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp]),

@@ -78,6 +78,35 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
     return target
 
 
+REFERENCE_SRC = Path("/root/reference/pkg")
+REFERENCE_TARGET = ROOT / "baseline" / "_ref"
+
+
+def install_reference(force: bool = False) -> Path | None:
+    """Install the unmodified reference ``kvsim`` into ``baseline/_ref`` (offline).
+
+    The engine and the out-of-scope harness modules execute the reference's own
+    sources (``_kvsim.py``); ``baseline/_ref`` is git-ignored but travels to the
+    GPU box with the repo snapshot.  Installed from a scratch copy because the
+    reference tree is read-only.  Returns the package directory, or None when
+    the reference tree is absent (GPU box: the snapshot already carries it).
+    """
+    pkg = REFERENCE_TARGET / "kvsim"
+    if (pkg / "engine.py").is_file() and not force:
+        return pkg
+    if not (REFERENCE_SRC / "pyproject.toml").is_file():
+        return None
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as tmp:
+        src = Path(tmp) / "pkg"
+        shutil.copytree(REFERENCE_SRC, src)
+        _run([sys.executable, "-m", "pip", "install", "--no-index", "--no-build-isolation",
+              "--no-deps", "--find-links", "/opt/wheelhouse", "--upgrade", "--target",
+              str(REFERENCE_TARGET), str(src)], False)
+    return pkg
+
+
 def _has_libcuda() -> bool:
     return False  # the driver entry point is resolved at run time (cudaGetDriverEntryPoint)
 

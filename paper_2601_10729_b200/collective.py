@@ -102,7 +102,9 @@ class SymmetricBuffers:
                 for r in range(world)]
 
     def next_epoch(self) -> int:
-        self.epoch = (self.epoch % 0xFFFFFFFF) + 1
+        # 1..0xFFFFFFFE: parity keeps alternating across the wrap (the inbox /
+        # flag slot is epoch & 1)
+        self.epoch = (self.epoch % 0xFFFFFFFE) + 1
         return self.epoch
 
     def check(self) -> None:

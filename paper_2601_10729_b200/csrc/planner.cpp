@@ -647,8 +647,13 @@ static int solve_ranked(const ofb_plan_problem* p, const Problem& P, Ranker& rk,
         if (p->parked_balance[j] - lat / tbt < 0.0) ++f;
       return f;
     };
+    // The stall model's completion slack (kSlackEps per layer, scaled by the
+    // window) can put a modelled latency below its bound by ~L*1e-9*(1+bound):
+    // test the bound minus that absolute margin so the cutoff never fires early.
+    const double slack_margin = (double)P.op.L * kSlackEps;
     rk.hopeless = [&](double bound) {
-      return (double)first_fails(bound * (1.0 - 1e-12)) > cap + kCapEps;
+      const double lo = bound * (1.0 - 1e-12) - slack_margin * (1.0 + bound);
+      return (double)first_fails(lo) > cap + kCapEps;
     };
     while (true) {
       Ranked cand;

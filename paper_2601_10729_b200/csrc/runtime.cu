@@ -597,10 +597,12 @@ int step_begin(ofb_runtime* rt, const ofb_step_desc* d, cudaStream_t cs) {
     if (rc) return rc;
     OFB_CUDA(cudaEventRecord(rec->start, cs));
   }
-  cudaError_t e = ofb::launch_kv_append(d->k_new, d->v_new, d->kv_pool, d->block_tables,
-                                        d->max_blocks, d->positions, d->host_slabs_dev, L, B,
-                                        d->num_kv_heads, /*kAppendResident*/ 0, cs);
-  if (e != cudaSuccess) return cuda_fail(e, "kv_append_kernel launch");
+  if (!d->append_per_layer) {
+    cudaError_t e = ofb::launch_kv_append(d->k_new, d->v_new, d->kv_pool, d->block_tables,
+                                          d->max_blocks, d->positions, d->host_slabs_dev, L, B,
+                                          d->num_kv_heads, /*kAppendResident*/ 0, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "kv_append_kernel launch");
+  }
   cudaEvent_t ev_start;
   rc = next_sync_event(rt, &ev_start);
   if (rc) return rc;
@@ -683,13 +685,13 @@ int step_layers(ofb_runtime* rt, int count) {
         layer_fetches = true;
       }
     }
-    if (layer_fetches) {
+    if (layer_fetches || d->append_per_layer) {
       const size_t kv_layer = (size_t)B * d->num_kv_heads * ofb::kHeadDim * 2;
       e = ofb::launch_kv_append(static_cast<const uint8_t*>(d->k_new) + l * kv_layer,
                                 static_cast<const uint8_t*>(d->v_new) + l * kv_layer, d->kv_pool,
                                 d->block_tables + l * bt_layer, d->max_blocks, d->positions,
                                 d->host_slabs_dev + (size_t)l * B, 1, B, d->num_kv_heads,
-                                /*kAppendOffloaded*/ 2, cs);
+                                d->append_per_layer ? /*kAppendAll*/ 1 : /*kAppendOffloaded*/ 2, cs);
       if (e != cudaSuccess) return cuda_fail(e, "kv_append_kernel launch");
     }
     cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -700,7 +702,7 @@ int step_layers(ofb_runtime* rt, int count) {
     // KV of a layer with no fetch this step was complete before the previous
     // layer's K1 passed its dependency wait (step-start append), so K1 may stream
     // it before its own wait; q / outputs / workspace still wait.
-    const bool kv_ready = l > 0 && !layer_fetches;
+    const bool kv_ready = l > 0 && !layer_fetches && !d->append_per_layer;
     e = ofb::launch_decode_attention(
         st.map, static_cast<const uint8_t*>(d->q) + l * q_layer,
         static_cast<uint8_t*>(d->out) + l * q_layer, d->block_tables + l * bt_layer, d->max_blocks,
@@ -807,6 +809,20 @@ int ofb_runtime_step_layers(ofb_runtime* rt, int32_t count) {
 int ofb_runtime_step_end(ofb_runtime* rt) {
   if (!rt) return fail(-1, "ofb_runtime_step_end: null runtime");
   return step_end(rt);
+}
+
+int ofb_runtime_step_abort(ofb_runtime* rt) {
+  if (!rt) return fail(-1, "ofb_runtime_step_abort: null runtime");
+  StepState& st = rt->step;
+  const bool was_active = st.active;
+  st.active = false;
+  if (!was_active && !rt->pf.valid) return 0;
+  if (st.cs) OFB_CUDA(cudaStreamSynchronize(st.cs));
+  for (auto s : rt->copy) OFB_CUDA(cudaStreamSynchronize(s));
+  rt->pf.valid = false;
+  rt->pf.entries.clear();
+  if (st.rec) st.rec->pending = false;
+  return 0;
 }
 
 int ofb_runtime_prefetch_stats(ofb_runtime* rt, int64_t* adopted, int64_t* dropped) {

@@ -23,6 +23,7 @@ KV values are synthetic (seeded N(0,1) bf16): there is no model checkpoint.
 from __future__ import annotations
 
 import math
+import time
 from collections import deque
 from dataclasses import dataclass, field
 
@@ -107,6 +108,7 @@ class B200Executor:
         self.last_inputs: dict | None = None
         self.last_output: torch.Tensor | None = None
         self.migrated = {"h2d_bytes": 0, "d2h_bytes": 0, "moves": 0}
+        self.prefill_wall_ms = 0.0
         self._ws = None
         self._mig_start = None        # event before the last un-stepped migration
         self._deferred: list = []     # evicted extents awaiting their D2H
@@ -127,6 +129,10 @@ class B200Executor:
         per_request = shape.num_layers * cap
         device_blocks = profile.gpu_block_budget + max_batch * per_request // 2 \
             + max_batch * staging_slots * cap + 64
+        # the engine keeps batch + paused <= max_batch (src/engine.py:478-504) and a
+        # restored layer's host slab is freed, so max_batch * per_request covers
+        # every host-resident slab; the factor 2 covers slabs deferred under an
+        # in-flight eviction
         host_blocks = 2 * max_batch * per_request + 64
         return cls(shape, device_blocks=device_blocks, host_blocks=host_blocks,
                    staging_slots=staging_slots, **kw)
@@ -142,6 +148,8 @@ class B200Executor:
         if tokens <= 0:
             return
         from . import ops
+
+        t0 = time.perf_counter()
 
         hkv = self.shape.num_kv_heads
         per_layer = tokens * hkv * HEAD_DIM * 2 * 2      # K + V bytes of one layer
@@ -159,26 +167,47 @@ class B200Executor:
                 v = torch.randn(shape, generator=g, device=self.device).to(torch.bfloat16)
             dst = torch.tensor(dsts[lo:hi], dtype=torch.int64).to(self.device)
             ops.kv_prefill(k, v, dst)
+        # host time of the prefill KV write: a live-wall engine clock excludes it
+        # (the reference already charges prefill, src/engine.py:495-503)
+        torch.cuda.current_stream().synchronize()
+        self.prefill_wall_ms += (time.perf_counter() - t0) * 1e3
 
     # ------------------------------------------------------------ HBM extents
     def _reclaim(self, wait: bool) -> None:
-        """Recycle extents evicted by earlier migrations once their D2H landed."""
+        """Recycle extents freed under an in-flight eviction once its D2H landed.
+
+        Evicted HBM extents (the D2H source) and host slabs of a request released
+        while an eviction may still be writing into them wait here; everything
+        else is stream-ordered after the restores (the compute stream waits for
+        them, and copy / migration streams start from the compute stream)."""
         if self._deferred and not self.runtime.migration_pending(wait=wait):
-            for start, cap in self._deferred:
-                self.pool.alloc.release(start, cap)
+            for alloc, start, cap in self._deferred:
+                alloc.release(start, cap)
             self._deferred.clear()
 
-    def _alloc_dev(self, n: int) -> int:
+    def _free(self, alloc, start: int, cap: int) -> None:
+        if self.runtime.migration_pending(wait=False):
+            self._deferred.append((alloc, start, cap))
+        else:
+            alloc.release(start, cap)
+
+    def _alloc(self, alloc, n: int) -> int:
         from .kvpool import PoolExhausted
 
         self._reclaim(wait=False)
         try:
-            return self.pool.alloc.alloc(n)
+            return alloc.alloc(n)
         except PoolExhausted:
             if not self._deferred:
                 raise
             self._reclaim(wait=True)
-            return self.pool.alloc.alloc(n)
+            return alloc.alloc(n)
+
+    def _alloc_dev(self, n: int) -> int:
+        return self._alloc(self.pool.alloc, n)
+
+    def _alloc_host(self, n: int) -> int:
+        return self._alloc(self.host.alloc, n)
 
     # ------------------------------------------------------------ table sync (K4)
     def _ensure(self, req: RequestState) -> _RequestSlabs:
@@ -217,7 +246,7 @@ class B200Executor:
         self.runtime.prefetch_fence()
         for rid in [r for r in self.slabs if r not in table.locations]:
             self.release(rid)
-        moves, evicted = [], []
+        moves, evicted, restored = [], [], []
         for rid, locs in table.locations.items():
             req = reqs.get(rid)
             if req is None:
@@ -232,7 +261,7 @@ class B200Executor:
                         st.dev[layer] = self._alloc_dev(st.capacity)
                         dsts.append(self.pool.addr(st.dev[layer]))
                     else:
-                        st.host[layer] = self.host.alloc.alloc(st.capacity)
+                        st.host[layer] = self._alloc_host(st.capacity)
                         dsts.append(self.host.addr(st.host[layer]))
                 self._prefill(rid, req.total_tokens, dsts)
                 continue
@@ -244,12 +273,17 @@ class B200Executor:
                     start = self._alloc_dev(st.capacity)
                     st.dev[layer] = start
                     moves.append((self.pool.addr(start), self.host.addr(st.host[layer]), nbytes, 0))
+                    # the host copy is dead once restored: later users of that range
+                    # (K5 on the compute stream, evictions, fetches) start after the
+                    # compute stream's wait for this restore
+                    restored.append((st.host[layer], st.capacity))
+                    st.host[layer] = None
                 elif loc not in _DEVICE_LOCS and on_dev:     # evict (D2H)
                     if st.host[layer] is None:
-                        st.host[layer] = self.host.alloc.alloc(st.capacity)
+                        st.host[layer] = self._alloc_host(st.capacity)
                     moves.append((self.host.addr(st.host[layer]), self.pool.addr(st.dev[layer]),
                                   nbytes, 1))
-                    evicted.append((st.dev[layer], st.capacity))
+                    evicted.append((self.pool.alloc, st.dev[layer], st.capacity))
                     st.dev[layer] = None
         if moves:
             if self._mig_start is None:
@@ -264,6 +298,10 @@ class B200Executor:
         # Evicted extents are recycled only once their D2H has landed (the
         # eviction overlaps the next step; see ofb_runtime_migrate).
         self._deferred.extend(evicted)
+        # Restored layers' host copies are dead; released only now, after the
+        # batch is issued, so nothing in this sync reuses a range a restore reads.
+        for start, cap in restored:
+            self.host.alloc.release(start, cap)
         self.layout_version += 1
 
     def install(self, batch: list[RequestState], placement: PlacementMatrix) -> None:
@@ -283,9 +321,9 @@ class B200Executor:
         for start in st.dev:
             if start is not None:
                 self.pool.alloc.release(start, st.capacity)
-        for start in st.host:
+        for start in st.host:      # an eviction may still be writing into these
             if start is not None:
-                self.host.alloc.release(start, st.capacity)
+                self._free(self.host.alloc, start, st.capacity)
         for start in st.staging:
             self.pool.alloc.release(start, st.capacity)
         self.layout_version += 1

@@ -44,6 +44,10 @@ class StepRuntime:
     def step_end(self) -> None:
         _native.check(self.lib.ofb_runtime_step_end(self.handle), "ofb_runtime_step_end")
 
+    def step_abort(self) -> None:
+        """Drop a step after a caller-side failure (never raises a second error)."""
+        self.lib.ofb_runtime_step_abort(self.handle)
+
     def prefetch_fence(self, stream=None) -> None:
         s = stream if stream is not None else torch.cuda.current_stream()
         _native.check(self.lib.ofb_runtime_prefetch_fence(self.handle, s.cuda_stream),

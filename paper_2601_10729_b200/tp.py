@@ -158,8 +158,10 @@ class TensorParallelDecoder:
             for l in range(L):
                 ex.runtime.step_layers(1)
                 self.proj(out, l, out=hidden[l], stream=stream)
-        finally:
-            ex.runtime.step_end()
+        except BaseException:
+            ex.runtime.step_abort()   # the original error propagates, not a step_end one
+            raise
+        ex.runtime.step_end()
         done = torch.cuda.Event()
         done.record(stream)
         ex.steps += 1
