@@ -51,9 +51,10 @@ CONFIGS = {
                   workload="Llama-3.1-8B shape, B=16, 32K ctx, every layer HBM-resident "
                            "(pure K1 chain; HBM-bound reference point for cfg2)"),
     "cfg4": dict(layers=80, hq=64, hkv=8, batch=32, prompt=65528, strides="flexgen_plus",
-                 output=64, hidden=8192,
-                 workload="Llama-3.1-70B shape (80 layers, 64q/8kv, d=128, bf16), B=32, 64K ctx, "
-                          "KV-head sharded TP, per-layer o-proj + all-reduce, plan = "
+                 output=64, hidden=8192, intermediate=28672,
+                 workload="Llama-3.1-70B shape (80 layers, 64q/8kv, d=128, hidden 8192, MLP 28672, "
+                          "bf16), B=32, 64K ctx, KV-head sharded TP, whole decoder step (QKV / "
+                          "o-proj / MLP weights streamed, o-proj and down-proj all-reduces), plan = "
                           "plan_flexgen_plus under each rank's HBM budget"),
 }
 
@@ -221,6 +222,15 @@ def _ncu_traffic(alg_bytes):
     return None
 
 
+def decoder_weight_bytes(cfg, shard) -> int:
+    """Bytes of one rank's weights for the whole-decoder step:
+    per layer q/k/v + o rows of its heads, and its 1/TP of gate/up/down."""
+    H, inter = cfg["hidden"], cfg["intermediate"] // shard.world
+    per_layer = ((shard.local_q + 2 * shard.local_kv) * 128 * H + shard.local_q * 128 * H
+                 + 3 * inter * H) * 2
+    return cfg["layers"] * per_layer
+
+
 def build_batch(cfg, shape=None, hbm_budget_bytes=None):
     """Batch + placement.  Fixed stride lists come from the config; "flexgen_plus"
     asks the reference-exact baseline planner (src/policies.py:132-137) for the
@@ -364,9 +374,14 @@ def run_ours(args, cfg):
     cap = -(-(cfg["prompt"] + cfg["output"] + 1) // 16)
     slots = args.staging_slots
     use_tp = world > 1 or args.tp_emulate > 1 or cfg["strides"] == "flexgen_plus"
-    # per-rank HBM left for KV: total - o-proj shard - staging - workspace/slack
+    full = (args.decoder or ("full" if "intermediate" in cfg else "attn")) == "full"
+    if full and "intermediate" not in cfg:
+        raise SystemExit(f"--decoder full needs an MLP shape; {args.config} is attention-only")
+    # per-rank HBM left for KV: total - weights (o-proj shard, or the whole decoder
+    # shard) - staging - workspace/slack
     free_b, _total_b = torch.cuda.mem_get_info(dev)
-    oproj_bytes = L * shard.local_q * 128 * cfg["hidden"] * 2 if use_tp else 0
+    oproj_bytes = (decoder_weight_bytes(cfg, shard) if full else
+                   L * shard.local_q * 128 * cfg["hidden"] * 2 if use_tp else 0)
     staging_bytes = B * slots * cap * shape.block_bytes
     kv_budget = free_b - oproj_bytes - staging_bytes - (6 << 30)
     if dist is not None:
@@ -402,15 +417,32 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
 
     inputs = [ex.synthetic_inputs(B, step=i) for i in range(2)]
-    pinned = [{k: v.cpu().pin_memory() for k, v in inp.items()} for inp in inputs]
-    out_host = torch.empty_like(inputs[0]["q"], device="cpu").pin_memory()
-
     attn_tokens = []
 
-    tpd = TensorParallelDecoder(ex, shard, cfg["hidden"], seed=0, max_batch=B) if use_tp else None
+    if full:
+        from paper_2601_10729_b200.tp import TensorParallelLlama
+
+        # whole decoder: the step's input is the new tokens' embeddings, its result
+        # the last hidden state; q / k_new / v_new come from the QKV projections
+        tpd = TensorParallelLlama(ex, shard, cfg["hidden"], cfg["intermediate"], c1=args.c1,
+                                  seed=0, max_batch=B)
+        g = torch.Generator(device=dev)
+        g.manual_seed(17)
+        step_in = [{"x": torch.randn((B, cfg["hidden"]), generator=g, device=dev).to(torch.bfloat16)}
+                   for _ in range(2)]
+        result = lambda: tpd.last_hidden  # noqa: E731
+    else:
+        tpd = TensorParallelDecoder(ex, shard, cfg["hidden"], seed=0, max_batch=B) if use_tp else None
+        step_in = inputs
+        result = lambda: ex.last_output  # noqa: E731
+    pinned = [{k: v.cpu().pin_memory() for k, v in inp.items()} for inp in step_in]
+    out_host = (torch.empty((B, cfg["hidden"]), dtype=torch.bfloat16) if full
+                else torch.empty_like(inputs[0]["q"], device="cpu")).pin_memory()
 
     def run_step(inp):
-        if tpd is not None:
+        if full:
+            tpd.step(batch, inp["x"])
+        elif tpd is not None:
             tpd.step(batch, inp)
         else:
             ex.decode_step(batch, None, inp, sync=False)
@@ -420,10 +452,10 @@ def run_ours(args, cfg):
         if e2e:   # a serving loop: inputs from host, result read back before the next step
             dev_in = {k: v.to(dev, non_blocking=True) for k, v in pinned[i % 2].items()}
             run_step(dev_in)
-            out_host.copy_(ex.last_output, non_blocking=True)
+            out_host.copy_(result(), non_blocking=True)
             torch.cuda.current_stream().synchronize()
         else:     # device-resident inputs, steps pipelined (host prepares N+1 during N)
-            run_step(inputs[i % 2])
+            run_step(step_in[i % 2])
         for r in batch:
             r.record_generated_token()
 
@@ -533,7 +565,8 @@ def run_ours(args, cfg):
 
     # step roofline: host link (HOST_alg) vs HBM (HBM_alg), SURVEY.md 8(d)
     host_alg = tm["acc_copy_bytes"] / tm["acc_steps"]
-    hbm_alg = L * attn_bytes + B * L * shape.kv_bytes_per_token
+    weight_bytes = tpd.weight_bytes if full else 0
+    hbm_alg = L * attn_bytes + B * L * shape.kv_bytes_per_token + weight_bytes
     roof_ms = max(hbm_alg / (hbm_peak * 1e9), host_alg / (h2d_peak * 1e9)) * 1e3
     copy_span = tm["copy_span_ms"]
     bound = "host_link" if host_alg / h2d_peak > hbm_alg / hbm_peak else "hbm"
@@ -565,11 +598,18 @@ def run_ours(args, cfg):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) KV, q)",
         "config": {"workload": cfg["workload"], "global_batch": B, "seq_len": cfg["prompt"],
                    "layers": L, "q_heads": hq_total, "kv_heads": hkv_total,
-                   "parallelism": (f"tp{world} (KV-head sharded; per layer K6: tcgen05 o-proj "
-                                   f"fused with a one-shot all-reduce over NVLink peer memory)"
+                   "parallelism": (f"tp{world} (KV-head sharded; C1 per layer: "
+                                   + ("K6, tcgen05 projection fused with a one-shot all-reduce over "
+                                      "NVLink peer memory)" if args.c1 == "k6" else
+                                      "cuBLAS projection + NCCL all-reduce)")
                                    if world > 1 else
-                                   f"tp{tp} rank-0 shard emulated on 1 GPU (K6 o-proj, no exchange)"
-                                   if tp > 1 else "single GPU"),
+                                   f"tp{tp} rank-0 shard emulated on 1 GPU ({args.c1} projections, "
+                                   "no exchange)" if tp > 1 else "single GPU"),
+                   "decoder": ("whole Llama layer per step: RMSNorm, QKV / gate-up (cuBLAS), K3+K1, "
+                               f"o-proj + down-proj with all-reduce ({args.c1}); "
+                               f"{weight_bytes / 1e9:.2f} GB of weights streamed per step"
+                               if full else "attention path (K3 + K2 + K1" +
+                               (" + K6 o-proj)" if tpd is not None else ")")),
                    "placement_rows_offloaded": [row.count(0) for row in placement.rows][:4],
                    "offloaded_slabs": n_off, "staging_slots": slots,
                    "copy_streams": tm["copy_streams"], "host_pipelining": "4 steps in flight",
@@ -611,9 +651,10 @@ def run_ours(args, cfg):
                           "blocks_to_fetch_check": blocks_to_fetch(placement, batch),
                           "per_copy_stream": _stream_summary(per_stream, PCIE5_NOMINAL_GBS, h2d_peak)},
         "attn_share_of_step": tm["acc_attn_ms"] / max(tm["acc_step_ms"], 1e-9),
-        "gpu_launches": args.steps * (1 + L + len({l for row in placement.rows
-                                                   for l, b in enumerate(row) if b == 0})
-                                      + (L if tpd is not None else 0)),
+        "gpu_launches": args.steps * ((L + L + (2 * L if args.c1 == "k6" else 0)) if full else
+                                      (1 + L + len({l for row in placement.rows
+                                                    for l, b in enumerate(row) if b == 0})
+                                       + (L if tpd is not None else 0))),
         "clocks": clocks.summary(),
     }
     if cpu is not None:
@@ -817,13 +858,171 @@ def run_cfg3(args):
     print(json.dumps(out), flush=True)
 
 
+def run_cfg4_serve(args):
+    """Config 4 through the serving engine: ``engine.Simulation`` drives one
+    KV-head-sharded rank per GPU (``tp.TensorParallelExecutor`` over the whole
+    decoder step, ``tp.TensorParallelLlama``), plans replicated on every rank
+    (C2).  Reports tokens/s, TPOT / TBT attainment and the binding roofline per
+    TP degree, in parity mode (decisions must equal the executor-less model run,
+    src/engine.py:706-734) and on the live-wall clock (solve + install + Python +
+    device step advance the clock).  Under torchrun every rank
+    runs the engine; alone, ``--tp-emulate N`` serves rank 0's shard of TP-N."""
+    import torch
+
+    from paper_2601_10729_b200 import defaults, workload
+    from paper_2601_10729_b200.calibrate import b200_profile
+    from paper_2601_10729_b200.core import RequestState
+    from paper_2601_10729_b200.engine import RunConfig, Simulation
+    from paper_2601_10729_b200.executor import B200Executor, ModelShape
+    from paper_2601_10729_b200.metrics import collect_metrics
+    from paper_2601_10729_b200.policies import PolicyKind, make_policy, plan_flexgen_plus
+    from paper_2601_10729_b200.tp import HeadShard, TensorParallelExecutor, TensorParallelLlama
+
+    cfg = CONFIGS["cfg4"]
+    rank, world, local = _env_rank()
+    local = local % max(1, torch.cuda.device_count())
+    dist = None
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist  # noqa: F811
+
+        dist.init_process_group(os.environ.get("OFB_DIST_BACKEND", "nccl"))
+    dev = torch.device("cuda", local)
+    tp = world if world > 1 else max(1, args.tp_emulate)
+    shard = HeadShard(rank if world > 1 else 0, tp, cfg["hq"], cfg["hkv"])
+    shape = ModelShape(cfg["layers"], shard.local_q, shard.local_kv)
+    L, B, P = cfg["layers"], cfg["batch"], cfg["prompt"]
+    outs = [args.cfg4_output + 2 * (i % 4) for i in range(B)]
+    trace = workload.Trace(tuple(workload.TraceRequest(0, P, o) for o in outs),
+                           {"config": "cfg4-serve"})
+    cap = -(-(P + max(outs) + 1) // 16)
+    slots = args.staging_slots
+    wbytes = decoder_weight_bytes(cfg, shard)
+    free_b, _ = torch.cuda.mem_get_info(dev)
+    kv_budget = free_b - wbytes - B * slots * cap * shape.block_bytes - (8 << 30)
+    if dist is not None:
+        t = torch.tensor([kv_budget], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        kv_budget = int(t.item())
+    budget = int(kv_budget // shape.block_bytes)
+    h2d_peak, d2h_peak = _probe_link(dev)
+    peaks = _measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6450.0)
+    # B200 cost model: the weight stream of a layer joins its fixed cost
+    layer_fixed = 0.012 + wbytes / L / (hbm_peak * 1e6)
+    profile = b200_profile(L, shard.local_kv, budget, h2d_gbs=h2d_peak, layer_fixed_ms=layer_fixed)
+    slo = defaults.default_slo(profile, scale=args.slo_scale)
+    run_cfg = RunConfig(max_batch=B, batch_token_cap=B * (P + max(outs)))
+    kind = PolicyKind(args.cfg4_policy)
+
+    def policy():
+        return make_policy(kind, profile, slo, max_batch=run_cfg.max_batch,
+                           token_cap=run_cfg.batch_token_cap)
+
+    head = {"metric": METRIC, "config": "cfg4-serve", "n_gpus": world, "tp": tp,
+            "workload": (f"Llama-3.1-70B shape, {B} requests x {P}-token prompts arriving at t=0, "
+                         f"outputs {min(outs)}-{max(outs)}, whole decoder step, policy {kind.value}"
+                         + ("" if world > 1 else f"; rank 0's shard of TP{tp} on one GPU")),
+            "policy": kind.value, "budget_blocks_per_rank": budget,
+            "block_bytes_per_rank": shape.block_bytes, "weight_bytes_per_rank": wbytes,
+            "slo": {"tpot_ms": slo.tpot_target_ms, "tbt_ms": slo.tbt_target_ms,
+                    "scale": args.slo_scale, "source": "defaults.default_slo(profile)"},
+            "profile": {"compute_base_ms": profile.compute_base_ms,
+                        "compute_per_token_ms": profile.compute_per_token_ms,
+                        "bandwidth_blocks_per_ms": profile.bandwidth_blocks_per_ms},
+            "h2d_peak_gbs": h2d_peak, "d2h_peak_gbs": d2h_peak, "hbm_peak_gbs": hbm_peak}
+    full_batch = [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=P,
+                               target_output_tokens=o) for i, o in enumerate(outs)]
+    first_plan = plan_flexgen_plus(full_batch, profile)
+    n_off = sum(row.count(0) for row in first_plan.rows)
+    host_need = n_off * cap * shape.block_bytes
+    avail = _mem_available() // max(1, world)
+    if host_need > 0.85 * avail:
+        if rank == 0:
+            print(json.dumps(dict(head, unavailable=(
+                f"needs {host_need / 2**30:.0f} GiB of pinned host KV per rank "
+                f"({n_off} offloaded slabs of {L * B}), {avail / 2**30:.0f} GiB available"))),
+                flush=True)
+        return
+    t0 = time.perf_counter()
+    model_log = Simulation(trace, policy(), profile, slo, run_cfg).execute()
+    model_s = time.perf_counter() - t0
+    ex = B200Executor(shape, device=dev, device_blocks=budget + B * slots * cap + 64,
+                      host_blocks=int(n_off * cap * 1.25) + 64, staging_slots=slots,
+                      copy_streams=args.copy_streams, seed=rank)
+    dec = TensorParallelLlama(ex, shard, cfg["hidden"], cfg["intermediate"], c1=args.c1,
+                              max_batch=B)
+    tex = TensorParallelExecutor(dec, seed=0)
+    out = dict(head, offloaded_slabs_first_plan=n_off,
+               host_control_ms_per_step_model=model_s * 1e3 / max(1, sum(
+                   r["kind"] == "step" for r in model_log)))
+    modes = [m.strip() for m in args.cfg4_modes.split(",") if m.strip()]
+    for mode in modes:
+        tex.steps = 0
+        with ClockSampler(local) as clocks:
+            t0 = time.perf_counter()
+            log = Simulation(trace, policy(), profile, slo, run_cfg, executor=tex,
+                             mode=mode).execute()
+            wall_s = time.perf_counter() - t0
+        steps = [r for r in log if r["kind"] == "step"]
+        gpu_ms = [r["payload"]["measured_us"] / 1e3 for r in steps]
+        tokens = sum(len(r["payload"]["ids"]) for r in steps)
+        rep = collect_metrics(log)
+        first = steps[0]["payload"]
+        rows, ids = first["rows"], first["ids"]
+        T = {r: P for r in ids}
+        host_alg = sum(row.count(0) * -(-T[i] // 16) for i, row in zip(ids, rows)) * shape.block_bytes
+        hbm_alg = (sum(row.count(1) * T[i] for i, row in zip(ids, rows)) * shape.kv_bytes_per_token
+                   + wbytes)
+        roof_ms = max(hbm_alg / (hbm_peak * 1e9), host_alg / (h2d_peak * 1e9)) * 1e3
+        span_us = steps[-1]["time_us"] + steps[-1]["payload"].get(
+            "wall_us", steps[-1]["payload"]["measured_us"]) - steps[0]["time_us"]
+        hist = {}
+        for r in steps:
+            hist[len(r["payload"]["ids"])] = hist.get(len(r["payload"]["ids"]), 0) + 1
+        rec = {"steps": len(steps), "tokens": tokens, "gpu_ms_total": sum(gpu_ms),
+               "tokens_per_s_device": tokens / (sum(gpu_ms) * 1e-3),
+               "tokens_per_s_clock": tokens / (span_us * 1e-6) if span_us > 0 else None,
+               "wall_s": wall_s, "step_ms_median": statistics.median(gpu_ms),
+               "tpot_attainment": rep.tpot_attainment, "tbt_attainment": rep.tbt_attainment,
+               "tpot_p95_ms": rep.tpot_p95_ms, "tbt_p95_ms": rep.tbt_p95_ms,
+               "batch_histogram": hist, "replans": rep.replans, "pauses": rep.pauses,
+               "preemptions": rep.preemptions, "migrated": dict(ex.migrated),
+               "first_step": {"offloaded_slabs": sum(row.count(0) for row in rows),
+                              "bound": "host_link" if host_alg / h2d_peak > hbm_alg / hbm_peak
+                              else "hbm",
+                              "host_alg_bytes": host_alg, "hbm_alg_bytes": hbm_alg,
+                              "roofline_ms": roof_ms, "measured_ms": gpu_ms[0],
+                              "achieved_frac": roof_ms / gpu_ms[0]},
+               "clocks": clocks.summary()}
+        if "wall_us" in steps[0]["payload"]:
+            walls = [r["payload"]["wall_us"] / 1e3 for r in steps]
+            rec["host_ms_per_step_median"] = statistics.median(
+                w - g for w, g in zip(walls, gpu_ms))
+        if mode == "parity":
+            stripped = [dict(r, payload={k: v for k, v in r["payload"].items()
+                                         if k not in ("measured_us", "wall_us")})
+                        if r["kind"] == "step" else r for r in log]
+            rec["decisions_match_model_run"] = stripped == model_log
+            rec["model_tpot_attainment"] = collect_metrics(model_log).tpot_attainment
+        out[mode] = rec
+        if rank == 0:
+            print(json.dumps({"mode": mode, **rec}), file=sys.stderr, flush=True)
+    tex.close()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS) + ["cfg3", "cfg3-policies", "cfg5"],
+    ap.add_argument("--config", choices=sorted(CONFIGS) + ["cfg3", "cfg3-policies", "cfg4-serve",
+                                                           "cfg5"],
                     default="cfg2")
     ap.add_argument("--slo-scale", type=float, default=1.5)
     ap.add_argument("--cfg3-requests", type=int, default=10)
@@ -843,11 +1042,25 @@ def main():
                          "which costs ~6%% on HBM-bound steps (cfg4, cfg2r)")
     ap.add_argument("--ref-seconds", type=float, default=3.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--decoder", choices=["attn", "full"], default=None,
+                    help="full: whole decoder step (QKV / MLP weights streamed); default full for "
+                         "cfg4, attention path for the others")
+    ap.add_argument("--c1", choices=["k6", "nccl"], default="k6",
+                    help="TP exchange: K6 (projection fused with the all-reduce over peer memory) "
+                         "or cuBLAS projection + NCCL all-reduce")
     ap.add_argument("--tp-emulate", type=int, default=1,
                     help="run rank 0's KV-head shard of a TP-N deployment on one GPU")
     ap.add_argument("--sweep-max-tokens", type=int, default=1048576,
                     help="cfg5: largest B x T swept (KV bytes = tokens x 128 KiB)")
+    ap.add_argument("--cfg4-output", type=int, default=16,
+                    help="cfg4-serve: output tokens per request (+0/2/4/6 by request)")
+    ap.add_argument("--cfg4-policy", default="flexgen_plus",
+                    help="cfg4-serve: a tractable plan source at B=32, L=80 (SURVEY.md 8(d))")
+    ap.add_argument("--cfg4-modes", default="parity,live-wall",
+                    help="cfg4-serve: engine clock modes to run (engine.MODES)")
     args = ap.parse_args()
+    if args.config == "cfg4-serve":
+        return run_cfg4_serve(args)
     if args.config == "cfg5":
         return run_reconfig(args)
     if args.config == "cfg3":

@@ -177,3 +177,271 @@ class TensorParallelDecoder:
             self.symm.check()
             self.symm.close()
             self.symm = None
+
+
+def _world(group) -> int:
+    import torch.distributed as dist
+
+    return dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+
+
+class TensorParallelLlama:
+    """One rank of a whole Llama decoder step, KV-head sharded.
+
+    Per layer, on one stream: input RMSNorm -> q / k / v projections of this
+    rank's heads (cuBLAS) -> K3 append of the fresh token + K2 fetch wait + K1
+    attention (the native step split per layer, ``append_per_layer``: k_new /
+    v_new of layer l only exist once layer l-1 finished) -> o-projection with
+    its all-reduce (C1) -> residual -> RMSNorm -> gate / up projection (cuBLAS)
+    -> SiLU * up -> down projection with its all-reduce -> residual.  So every
+    weight byte of the 70B shard is streamed from HBM each step (137 GB / TP),
+    and the step time is the real decoder's, not attention alone.
+
+    ``c1="k6"``: both reductions are K6 (``collective.OprojAllReduce``: tcgen05
+    projection fused with the one-shot all-reduce over IPC peer memory; the
+    down projection has the same shape class).  ``c1="nccl"``: cuBLAS
+    projection + ``torch.distributed.all_reduce`` (NCCL over NVLink) - the
+    unfused baseline the north star names.  With world 1 (a
+    TP-N shard emulated on one GPU) there is no exchange in either arm.
+    Weights are random bf16 (no checkpoint), scaled 1/sqrt(fan_in); norms are
+    unit-weight.
+    """
+
+    def __init__(self, executor, shard: HeadShard, hidden: int, intermediate: int, *,
+                 c1: str = "k6", group=None, seed: int = 0, max_batch: int = 256,
+                 eps: float = 1e-5):
+        from .collective import OprojAllReduce, SymmetricBuffers
+
+        if c1 not in ("k6", "nccl"):
+            raise ValueError("c1 must be 'k6' or 'nccl'")
+        if intermediate % shard.world:
+            raise ValueError("intermediate size must divide by the TP degree")
+        ex = self.ex = executor
+        self.shard, self.hidden, self.group, self.c1, self.eps = shard, hidden, group, c1, eps
+        L, dev = ex.shape.num_layers, ex.device
+        hq, hkv = shard.local_q, shard.local_kv
+        self.inter = intermediate // shard.world
+        self.world = _world(group)
+        if self.world > 1 and self.world != shard.world:
+            raise ValueError("process group size differs from the head shard's world")
+        g = torch.Generator(device=dev)
+        g.manual_seed(7001 + 131 * seed + shard.rank)
+
+        def rand(shape, fan_in):
+            out = torch.empty(shape, dtype=torch.bfloat16, device=dev)
+            for l in range(shape[0]):
+                out[l] = (torch.randn(shape[1:], generator=g, device=dev) * fan_in ** -0.5).to(
+                    torch.bfloat16)
+            return out
+
+        qkv_rows = (hq + 2 * hkv) * 128
+        self.w_qkv = rand((L, qkv_rows, hidden), hidden)            # Linear layout [out, in]
+        self.w_gu = rand((L, 2 * self.inter, hidden), hidden)
+        w_o = rand((L, hidden, hq * 128), shard.num_q_heads * 128)
+        w_d = rand((L, hidden, self.inter), intermediate)
+        self.norm = torch.ones((2, hidden), dtype=torch.bfloat16, device=dev)
+        self.symm = None
+        if c1 == "k6":
+            if self.world > 1:
+                self.symm = SymmetricBuffers(self.world, shard.rank, max_batch, hidden, group=group,
+                                             device=dev)
+            self.oproj = OprojAllReduce(w_o, max_batch, self.symm)
+            self.down = OprojAllReduce(w_d, max_batch, self.symm)
+            del w_o, w_d
+        else:
+            self.w_o, self.w_d = w_o, w_d
+        self.max_batch = max_batch
+        self._bufs = None
+        self.last_hidden = None
+
+    def layer_weights(self, l: int) -> dict:
+        """Layer ``l``'s weights in ``nn.Linear`` layout [out, in] (test / reference use)."""
+        nq, nk = self.shard.local_q * 128, self.shard.local_kv * 128
+        w = self.w_qkv[l]
+
+        def unpack(proj):
+            t = proj.w[l]
+            if proj.w_layout == 0:
+                return t
+            tiles, chunks = t.shape[:2]
+            return t.permute(0, 2, 1, 3).reshape(tiles * 128, chunks * 64)
+
+        o = unpack(self.oproj) if self.c1 == "k6" else self.w_o[l]
+        d = unpack(self.down) if self.c1 == "k6" else self.w_d[l]
+        return {"q": w[:nq], "k": w[nq:nq + nk], "v": w[nq + nk:], "o": o,
+                "gate": self.w_gu[l, : self.inter], "up": self.w_gu[l, self.inter:], "down": d}
+
+    @property
+    def weight_bytes(self) -> int:
+        """Bytes of weights one step streams (every layer's projections)."""
+        L = self.ex.shape.num_layers
+        per_layer = ((self.w_qkv[0].numel() + self.w_gu[0].numel())
+                     + self.hidden * (self.shard.local_q * 128 + self.inter)) * 2
+        return L * per_layer
+
+    def _buffers(self, B: int):
+        if self._bufs is None or self._bufs["B"] != B:
+            L, dev = self.ex.shape.num_layers, self.ex.device
+            hq, hkv = self.shard.local_q, self.shard.local_kv
+            mk = lambda *s: torch.empty(s, dtype=torch.bfloat16, device=dev)  # noqa: E731
+            self._bufs = {"B": B, "q": mk(L, B, hq, 128), "k_new": mk(L, B, hkv, 128),
+                          "v_new": mk(L, B, hkv, 128), "act": mk(L, B, self.inter),
+                          "h": mk(B, self.hidden), "x": [mk(B, self.hidden), mk(B, self.hidden)]}
+        return self._bufs
+
+    def _reduce(self, proj, w, x_all, l, out, stream):
+        """out = sum over ranks of x_all[l] @ w[l]^T (C1)."""
+        if self.c1 == "k6":
+            proj(x_all, l, out=out, stream=stream)
+            return
+        torch.matmul(x_all[l].reshape(out.shape[0], -1), w[l].t(), out=out)
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(out, group=self.group)
+
+    def step(self, batch, x_in: torch.Tensor) -> torch.Tensor:
+        """One decode step of the whole decoder; ``x_in`` bf16 [B, hidden] (the
+        new tokens' embeddings).  Returns the final hidden state [B, hidden]."""
+        import torch.nn.functional as F
+
+        ex = self.ex
+        B, L = len(batch), ex.shape.num_layers
+        if B > self.max_batch:
+            raise ValueError("batch exceeds max_batch")
+        bufs = self._buffers(B)
+        q, kn, vn = bufs["q"], bufs["k_new"], bufs["v_new"]
+        desc, keep = ex.prepare_step(batch, {"q": q, "k_new": kn, "v_new": vn})
+        desc.append_per_layer = 1
+        out = keep[1]
+        stream = torch.cuda.current_stream()
+        x = bufs["x"][ex.steps % 2]
+        x.copy_(x_in)
+        h = bufs["h"]
+        nq, nk = self.shard.local_q * 128, self.shard.local_kv * 128
+        ex.runtime.step_begin(desc, stream)
+        try:
+            for l in range(L):
+                a = F.rms_norm(x, (self.hidden,), self.norm[0], self.eps)
+                w = self.w_qkv[l]
+                torch.matmul(a, w[:nq].t(), out=q[l].view(B, nq))
+                torch.matmul(a, w[nq:nq + nk].t(), out=kn[l].view(B, nk))
+                torch.matmul(a, w[nq + nk:].t(), out=vn[l].view(B, nk))
+                ex.runtime.step_layers(1)                    # K3 + K2 wait + K1 of layer l
+                self._reduce(getattr(self, "oproj", None), getattr(self, "w_o", None), out, l, h,
+                             stream)
+                x.add_(h)
+                a = F.rms_norm(x, (self.hidden,), self.norm[1], self.eps)
+                gu = torch.matmul(a, self.w_gu[l].t())
+                torch.mul(F.silu(gu[:, : self.inter]), gu[:, self.inter:], out=bufs["act"][l])
+                self._reduce(getattr(self, "down", None), getattr(self, "w_d", None), bufs["act"],
+                             l, h, stream)
+                x.add_(h)
+        except BaseException:
+            ex.runtime.step_abort()
+            raise
+        ex.runtime.step_end()
+        done = torch.cuda.Event()
+        done.record(stream)
+        ex.steps += 1
+        ex.last_inputs, ex.last_output = {"q": q, "k_new": kn, "v_new": vn}, out
+        ex._inflight.append((done, keep))
+        while len(ex._inflight) > 3:
+            ex._inflight.popleft()[0].synchronize()
+        self.last_hidden = x
+        return x
+
+    def close(self) -> None:
+        if self.symm is not None:
+            self.symm.check()
+            self.symm.close()
+            self.symm = None
+
+
+class TensorParallelExecutor:
+    """The engine seam (``sync_table`` / ``decode_step`` / ``release``, as
+    ``executor.B200Executor``) for one rank of a KV-head-sharded deployment, so
+    ``engine.Simulation`` drives a TP run (src/engine.py:708-734).
+
+    Every rank runs its own engine; plans are pure functions of the batch
+    (S:254), so the ranks compute the same placement (C2) - verified with one
+    digest all-gather whenever the placement changes.  A step
+    lasts as long as its slowest rank, so the device time a live clock sees is
+    the max over ranks (one tiny all-reduce), which keeps the ranks' engines in
+    lock step in every clock mode."""
+
+    def __init__(self, decoder: TensorParallelLlama, group=None, seed: int = 0):
+        self.dec = decoder
+        self.ex = decoder.ex
+        self.group = group
+        self.seed = seed
+        self.world = _world(group)
+        self._rows = None
+        self.steps = 0
+        self.last_ms = None
+
+    @property
+    def prefill_wall_ms(self) -> float:
+        return self.ex.prefill_wall_ms
+
+    @property
+    def migrated(self):
+        return self.ex.migrated
+
+    @property
+    def runtime(self):
+        return self.ex.runtime
+
+    def sync_table(self, table, batch, paused=()) -> None:
+        self.ex.sync_table(table, batch, paused)
+
+    def release(self, rid: int) -> None:
+        self.ex.release(rid)
+
+    def embeddings(self, B: int) -> torch.Tensor:
+        """Seeded stand-in for this step's token embeddings (same on every rank)."""
+        g = torch.Generator(device=self.ex.device)
+        g.manual_seed(90001 + 7919 * self.seed + self.steps)
+        return torch.randn((B, self.dec.hidden), generator=g, device=self.ex.device).to(
+            torch.bfloat16)
+
+    def decode_step(self, batch, placement=None) -> float:
+        ex = self.ex
+        if placement is not None:
+            rows = tuple(tuple(r) for r in placement.rows)
+            if rows != self._rows:
+                if not check_plan_replicated(rows, self.group):
+                    raise RuntimeError("ranks computed different placements (C2 violated)")
+                self._rows = rows
+            for req, row in zip(batch, placement.rows):
+                st = ex.slabs.get(req.id)
+                if st is None or any((st.dev[l] is not None) != bool(b) for l, b in enumerate(row)):
+                    raise RuntimeError("physical residency does not match the placement")
+        x0 = self.embeddings(len(batch))
+        stream = torch.cuda.current_stream()
+        t1 = torch.cuda.Event(enable_timing=True)
+        if ex._mig_start is not None:      # the step also waits for its plan's migration
+            t0, ex._mig_start = ex._mig_start, None
+        else:
+            t0 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+        self.dec.step(batch, x0)
+        t1.record(stream)
+        t1.synchronize()
+        ex._inflight.clear()
+        self.steps += 1
+        ms = t0.elapsed_time(t1)
+        if self.world > 1:
+            import torch.distributed as dist
+
+            t = torch.tensor([ms], dtype=torch.float64)
+            if dist.get_backend(self.group) == "nccl":
+                t = t.to(ex.device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+            ms = float(t.item())
+        self.last_ms = ms
+        return ms
+
+    def close(self) -> None:
+        self.dec.close()
+        self.ex.close()

@@ -1,0 +1,261 @@
+"""The whole-decoder TP step (cfg4), the engine-driven TP executor, the
+live-wall clock and step abort.
+
+* ``TensorParallelLlama``: every layer's attention vs the CPU oracle (q from the
+  QKV projection, KV from the slabs), the per-layer K3 append bit-exact against
+  the projected k/v, and the whole hidden-state chain vs an fp32 torch
+  restatement of the decoder layer (the attention output fed in from the GPU,
+  itself checked against the oracle).
+* ``TensorParallelExecutor`` under ``engine.Simulation``: parity-mode decisions
+  equal the executor-less model run (src/engine.py:706-734).
+* live-wall: a slow solve shifts the engine clock and the deliveries
+  (src/engine.py:82-123, :612-632).
+* a caller-side failure inside a split step propagates unchanged and leaves the
+  runtime usable (``ofb_runtime_step_abort``).
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+from paper_2601_10729_b200 import workload
+from paper_2601_10729_b200.core import PlacementMatrix, RequestState, SloConfig, SystemProfile
+from paper_2601_10729_b200.engine import RunConfig, Simulation
+from paper_2601_10729_b200.policies import PolicyKind, make_policy
+
+from test_executor_gpu import _check_step_outputs
+
+pytestmark = pytest.mark.gpu
+
+
+def _decoder(c1, L=3, hq=8, hkv=2, hidden=256, inter=512, B=3, seed=0, dev_extra=0):
+    from paper_2601_10729_b200.executor import B200Executor, ModelShape
+    from paper_2601_10729_b200.tp import HeadShard, TensorParallelLlama
+
+    shape = ModelShape(L, hq, hkv)
+    ex = B200Executor(shape, device_blocks=L * B * 40 + 2 * B * 40 + 64 + dev_extra,
+                      host_blocks=L * B * 40 + 64, staging_slots=2, record_timing=True, seed=seed)
+    dec = TensorParallelLlama(ex, HeadShard(0, 1, hq, hkv), hidden, inter, c1=c1, seed=seed,
+                              max_batch=B)
+    return ex, dec
+
+
+def _batch(B=3):
+    return [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=150 + 61 * i,
+                         target_output_tokens=20) for i in range(B)]
+
+
+def _rms(x, eps=1e-5):
+    return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + eps)
+
+
+def _reference_chain(dec, ex, x_in):
+    """fp32 decoder chain with the GPU attention output of every layer fed in."""
+    L, B = ex.shape.num_layers, x_in.shape[0]
+    x = x_in.float()
+    qkv = []
+    for l in range(L):
+        w = {k: v.float() for k, v in dec.layer_weights(l).items()}
+        a = _rms(x)
+        qkv.append((a @ w["q"].t(), a @ w["k"].t(), a @ w["v"].t()))
+        att = ex.last_output[l].float().reshape(B, -1)
+        x = x + att @ w["o"].t()
+        a = _rms(x)
+        x = x + (F.silu(a @ w["gate"].t()) * (a @ w["up"].t())) @ w["down"].t()
+    return x, qkv
+
+
+@pytest.mark.parametrize("c1", ["k6", "nccl"])
+def test_llama_decoder_step(c1):
+    ex, dec = _decoder(c1)
+    batch = _batch()
+    L = ex.shape.num_layers
+    rows = ((1, 0, 1), (0, 0, 0), (1, 1, 1))           # mixed resident / host-resident
+    placement = PlacementMatrix(tuple(r.id for r in batch), L, rows)
+    try:
+        ex.install(batch, placement)
+        g = torch.Generator(device=ex.device)
+        g.manual_seed(5)
+        for step in range(3):
+            x_in = torch.randn((len(batch), dec.hidden), generator=g, device=ex.device).to(
+                torch.bfloat16)
+            out = dec.step(batch, x_in)
+            torch.cuda.synchronize()
+            ex.last_positions = np.array([r.total_tokens for r in batch], dtype=np.int32)
+            _check_step_outputs(ex, batch)          # K1 vs oracle, q from the projection
+            want, qkv = _reference_chain(dec, ex, x_in)
+            q = ex.last_inputs["q"].float()
+            kn, vn = ex.last_inputs["k_new"], ex.last_inputs["v_new"]
+            for l in range(L):
+                B = len(batch)
+                torch.testing.assert_close(q[l].reshape(B, -1), qkv[l][0], rtol=3e-2, atol=3e-2)
+                torch.testing.assert_close(kn[l].float().reshape(B, -1), qkv[l][1], rtol=3e-2,
+                                           atol=3e-2)
+                # K3 ran per layer: the token's slot holds the projected k / v bit for bit
+                for b, r in enumerate(batch):
+                    pos = r.total_tokens
+                    bits = ex.slab_bits(r.id, l, pos // 16 + 1)
+                    kb = kn[l, b].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+                    vb = vn[l, b].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+                    np.testing.assert_array_equal(bits[pos // 16, :, 0, pos % 16], kb)
+                    np.testing.assert_array_equal(bits[pos // 16, :, 1, pos % 16], vb)
+            torch.testing.assert_close(out.float(), want, rtol=5e-2, atol=5e-2)
+            assert torch.isfinite(out.float()).all()
+            for r in batch:
+                r.record_generated_token()
+    finally:
+        dec.close()
+        ex.close()
+
+
+def test_c1_arms_agree():
+    """K6 (fused projection) and the cuBLAS arm give the same decoder (world 1)."""
+    outs = []
+    for c1 in ("k6", "nccl"):
+        ex, dec = _decoder(c1, seed=3)
+        batch = _batch()
+        placement = PlacementMatrix(tuple(r.id for r in batch), 3, ((1, 1, 1),) * 3)
+        ex.install(batch, placement)
+        x = torch.ones((3, dec.hidden), dtype=torch.bfloat16, device=ex.device)
+        outs.append(dec.step(batch, x).float().clone())
+        torch.cuda.synchronize()
+        dec.close()
+        ex.close()
+    torch.testing.assert_close(outs[0], outs[1], rtol=3e-2, atol=3e-2)
+
+
+def _toy_engine():
+    prof = SystemProfile(num_layers=4, compute_base_ms=0.2, compute_per_token_ms=0.0004,
+                         bandwidth_blocks_per_ms=12.0, gpu_block_budget=120, block_size=16,
+                         prefill_per_token_ms=0.001)
+    slo = SloConfig(tbt_target_ms=2.5, tpot_target_ms=2.5, window_min=2, window_max=6)
+    trace = workload.Trace(tuple(workload.TraceRequest(i * 3, 90 + 37 * i, 6 + i % 3)
+                                 for i in range(6)), {})
+    return prof, slo, trace, RunConfig(max_batch=3)
+
+
+def _strip(log):
+    return [dict(r, payload={k: v for k, v in r["payload"].items()
+                             if k not in ("measured_us", "wall_us")})
+            if r["kind"] == "step" else r for r in log]
+
+
+def test_tp_executor_under_engine():
+    from paper_2601_10729_b200.executor import B200Executor, ModelShape
+    from paper_2601_10729_b200.tp import HeadShard, TensorParallelExecutor, TensorParallelLlama
+
+    prof, slo, trace, cfg = _toy_engine()
+
+    def policy():
+        return make_policy(PolicyKind.ORBIT, prof, slo, max_batch=3, token_cap=cfg.batch_token_cap)
+
+    model = Simulation(trace, policy(), prof, slo, cfg).execute()
+    ex = B200Executor.for_trace(trace, prof, shape=ModelShape(4, 8, 2), max_batch=3)
+    dec = TensorParallelLlama(ex, HeadShard(0, 1, 8, 2), 256, 512, max_batch=3)
+    tex = TensorParallelExecutor(dec)
+    try:
+        log = Simulation(trace, policy(), prof, slo, cfg, executor=tex).execute()
+        assert _strip(log) == model
+        steps = [r for r in log if r["kind"] == "step"]
+        assert tex.steps == len(steps) and all(r["payload"]["measured_us"] > 0 for r in steps)
+        assert not ex.slabs                       # every finished request was released
+        wall = Simulation(trace, policy(), prof, slo, cfg, executor=tex, mode="live-wall").execute()
+        wsteps = [r for r in wall if r["kind"] == "step"]
+        assert all(r["payload"]["wall_us"] >= r["payload"]["measured_us"] for r in wsteps)
+        assert sum(r["kind"] == "finish" for r in wall) == len(trace.requests)
+    finally:
+        tex.close()
+
+
+def test_live_wall_slow_solve_shifts_deliveries(monkeypatch):
+    """A solve that takes 40 ms of host time delays the next step by as much on the
+    live-wall clock (and not on the live-device clock)."""
+    from paper_2601_10729_b200 import engine
+    from paper_2601_10729_b200.executor import B200Executor, ModelShape
+
+    prof, slo, trace, cfg = _toy_engine()
+
+    def run(mode):
+        ex = B200Executor.for_trace(trace, prof, shape=ModelShape(4, 8, 2), max_batch=3)
+        policy = make_policy(PolicyKind.ORBIT, prof, slo, max_batch=3, token_cap=cfg.batch_token_cap)
+        log = Simulation(trace, policy, prof, slo, cfg, executor=ex, mode=mode).execute()
+        ex.close()
+        return log
+
+    fast = run("live-wall")
+    solves = [0]
+    real_solve = engine._ref.solve
+
+    def slow_solve(*a, **kw):
+        import time
+
+        solves[0] += 1
+        time.sleep(0.04)
+        return real_solve(*a, **kw)
+
+    monkeypatch.setattr(engine._ref, "solve", slow_solve)
+    slow = run("live-wall")
+    device = run("live")
+    assert solves[0] > 0
+
+    def last_delivery(log):
+        return max(r["time_us"] for r in log if r["kind"] == "deliver")
+
+    def replan_steps(log):
+        out, pending = [], False
+        for r in log:
+            if r["kind"] == "replan":
+                pending = True
+            elif r["kind"] == "step":
+                if pending:
+                    out.append(r["payload"]["wall_us"])
+                pending = False
+        return out
+
+    # every step that followed a solve carries its 40 ms on the wall clock
+    assert min(replan_steps(slow)) >= 40_000
+    assert last_delivery(slow) - last_delivery(fast) >= 0.5 * 40_000 * len(replan_steps(slow))
+    # the device clock does not see host time
+    assert max(r["payload"]["measured_us"] for r in device if r["kind"] == "step") < 40_000
+
+
+def test_step_abort_keeps_runtime_usable():
+    from paper_2601_10729_b200.executor import B200Executor, ModelShape
+    from paper_2601_10729_b200.tp import HeadShard, TensorParallelDecoder
+
+    shape = ModelShape(3, 8, 2)
+    batch = _batch()
+    ex = B200Executor(shape, device_blocks=3 * 3 * 40 + 6 * 40 + 64, host_blocks=3 * 3 * 40 + 64,
+                      staging_slots=2, record_timing=True)
+    placement = PlacementMatrix(tuple(r.id for r in batch), 3, ((1, 0, 1), (0, 0, 0), (1, 1, 1)))
+    tpd = TensorParallelDecoder(ex, HeadShard(0, 1, 8, 2), hidden=256, max_batch=3)
+    try:
+        ex.install(batch, placement)
+        real = tpd.proj
+
+        class Boom(RuntimeError):
+            pass
+
+        calls = [0]
+
+        def failing(*a, **kw):
+            calls[0] += 1
+            if calls[0] == 2:
+                raise Boom("projection failed")
+            return real(*a, **kw)
+
+        tpd.proj = failing
+        with pytest.raises(Boom):
+            tpd.step(batch, ex.synthetic_inputs(3, step=0))
+        tpd.proj = real
+        ex.drain()
+        tpd.step(batch, ex.synthetic_inputs(3, step=1))
+        torch.cuda.synchronize()
+        ex.last_positions = np.array([r.total_tokens for r in batch], dtype=np.int32)
+        _check_step_outputs(ex, batch)
+    finally:
+        tpd.close()
+        ex.close()
