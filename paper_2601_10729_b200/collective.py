@@ -137,6 +137,13 @@ class SymmetricBuffers:
         return [self.local]
 
 
+def pack_weight(w: torch.Tensor) -> torch.Tensor:
+    """[..., H, K] (nn.Linear layout) -> [..., H/128, K/64, 128, 64]: every 128 x 64
+    tile K6's TMA loads is 16 KiB contiguous."""
+    *lead, h, k = w.shape
+    return (w.reshape(*lead, h // 128, 128, k // 64, 64).transpose(-3, -2).contiguous())
+
+
 class OprojAllReduce:
     """K6: ``hidden[B, H] = sum over ranks of x_r[B, K] @ W_r[H, K]^T`` per layer.
 
@@ -147,19 +154,23 @@ class OprojAllReduce:
 
     def __init__(self, w_o: torch.Tensor, max_batch: int, symm: SymmetricBuffers | None = None,
                  timeout_ns: int = 0, pack: bool = True):
-        if not w_o.is_cuda or w_o.dtype != torch.bfloat16 or w_o.dim() != 3:
-            raise ValueError("w_o must be a bf16 CUDA tensor [layers, hidden, k]")
-        self.layers, self.hidden, self.k = w_o.shape
-        if self.k % 64 or self.hidden % 128:
-            raise ValueError("k must be a multiple of 64 and hidden of 128")
-        # Weights are static: pack once so that every TMA box the kernel loads
-        # (128 rows x 64 k of one hidden tile) is 16 KiB contiguous in HBM.
-        self.w_layout = 1 if pack else 0
-        if pack:
-            self.w = (w_o.reshape(self.layers, self.hidden // 128, 128, self.k // 64, 64)
-                      .permute(0, 1, 3, 2, 4).contiguous())
+        if not w_o.is_cuda or w_o.dtype != torch.bfloat16 or w_o.dim() not in (3, 5):
+            raise ValueError("w_o must be a bf16 CUDA tensor [layers, hidden, k] "
+                             "(or already packed: [layers, hidden/128, k/64, 128, 64])")
+        if w_o.dim() == 5:      # packed by the caller (see pack_weight)
+            if tuple(w_o.shape[3:]) != (128, 64) or not w_o.is_contiguous():
+                raise ValueError("a packed w_o must be contiguous [layers, hidden/128, k/64, 128, 64]")
+            self.layers, tiles, chunks = w_o.shape[:3]
+            self.hidden, self.k = tiles * 128, chunks * 64
+            self.w_layout, self.w = 1, w_o
         else:
-            self.w = w_o.contiguous()
+            self.layers, self.hidden, self.k = w_o.shape
+            if self.k % 64 or self.hidden % 128:
+                raise ValueError("k must be a multiple of 64 and hidden of 128")
+            # Weights are static: pack once so that every TMA box the kernel loads
+            # (128 rows x 64 k of one hidden tile) is 16 KiB contiguous in HBM.
+            self.w_layout = 1 if pack else 0
+            self.w = pack_weight(w_o) if pack else w_o.contiguous()
         if symm is not None and (symm.hidden != self.hidden or symm.max_batch < max_batch):
             raise ValueError("symmetric buffers sized for another hidden / batch")
         self.max_batch = max_batch

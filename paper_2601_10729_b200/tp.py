@@ -227,18 +227,25 @@ class TensorParallelLlama:
         g = torch.Generator(device=dev)
         g.manual_seed(7001 + 131 * seed + shard.rank)
 
-        def rand(shape, fan_in):
-            out = torch.empty(shape, dtype=torch.bfloat16, device=dev)
-            for l in range(shape[0]):
-                out[l] = (torch.randn(shape[1:], generator=g, device=dev) * fan_in ** -0.5).to(
-                    torch.bfloat16)
+        from .collective import pack_weight
+
+        def rand(shape, fan_in, packed=False):
+            """Random bf16 layers, generated one layer at a time (no full-size
+            temporaries: the 70B shard fills most of HBM); ``packed``: K6 layout."""
+            L_, h, k = shape
+            out = torch.empty((L_, h // 128, k // 64, 128, 64) if packed else shape,
+                              dtype=torch.bfloat16, device=dev)
+            for l in range(L_):
+                w = (torch.randn((h, k), generator=g, device=dev) * fan_in ** -0.5).to(torch.bfloat16)
+                out[l] = pack_weight(w) if packed else w
             return out
 
         qkv_rows = (hq + 2 * hkv) * 128
         self.w_qkv = rand((L, qkv_rows, hidden), hidden)            # Linear layout [out, in]
         self.w_gu = rand((L, 2 * self.inter, hidden), hidden)
-        w_o = rand((L, hidden, hq * 128), shard.num_q_heads * 128)
-        w_d = rand((L, hidden, self.inter), intermediate)
+        packed = c1 == "k6"
+        w_o = rand((L, hidden, hq * 128), shard.num_q_heads * 128, packed)
+        w_d = rand((L, hidden, self.inter), intermediate, packed)
         self.norm = torch.ones((2, hidden), dtype=torch.bfloat16, device=dev)
         self.symm = None
         if c1 == "k6":
