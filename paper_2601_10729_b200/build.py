@@ -78,6 +78,42 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
     return target
 
 
+TORCH_OPS_NAME = "liborbit_torch_ops.so"
+
+
+def torch_ops_path() -> Path:
+    return OUT_DIR / TORCH_OPS_NAME
+
+
+def build_torch_ops(verbose: bool = False, force: bool = False) -> Path:
+    """The ``orbit::`` torch.library registration (csrc/torch_ops.cpp): host-only
+    C++ against torch's headers, linked to liborbitflow_b200.so (found next to it
+    through $ORIGIN), so ``torch.ops.orbit.*`` and the ctypes binding call the same
+    kernels.  Plain g++ - no JIT cache, the .so stays in-tree and travels."""
+    from torch.utils import cpp_extension
+
+    lib = build(verbose=verbose)
+    target = torch_ops_path()
+    src = CSRC / "torch_ops.cpp"
+    if not force and not _stale(target, [src, lib, ROOT / "include" / "orbitflow_b200.h"]):
+        return target
+    import torch
+
+    incs = [f"-I{p}" for p in cpp_extension.include_paths(device_type="cuda")]
+    libdirs = cpp_extension.library_paths(device_type="cuda")
+    abi = int(torch._C._GLIBCXX_USE_CXX11_ABI)
+    tmp = target.with_suffix(".so.tmp")
+    cmd = [os.environ.get("CXX", "g++"), "-O2", "-std=c++17", "-shared", "-fPIC",
+           f"-D_GLIBCXX_USE_CXX11_ABI={abi}", "-DTORCH_EXTENSION_NAME=orbit_torch_ops",
+           f"-I{ROOT / 'include'}", *incs, str(src), "-o", str(tmp),
+           f"-L{OUT_DIR}", "-l:" + LIB_NAME, "-Wl,-rpath,$ORIGIN",
+           *[f"-L{d}" for d in libdirs], "-lc10", "-lc10_cuda", "-ltorch_cpu", "-ltorch_cuda",
+           "-ltorch", "-ltorch_python"]
+    _run(cmd, verbose)
+    os.replace(tmp, target)
+    return target
+
+
 REFERENCE_SRC = Path("/root/reference/pkg")
 REFERENCE_TARGET = ROOT / "baseline" / "_ref"
 
@@ -118,7 +154,7 @@ def _run(cmd, verbose):
     if verbose and res.stderr:
         print(res.stderr, file=sys.stderr)
     if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+        raise RuntimeError(f"build step failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
 
 
 if __name__ == "__main__":

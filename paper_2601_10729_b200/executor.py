@@ -82,7 +82,7 @@ class B200Executor:
     def __init__(self, shape: ModelShape, *, device_blocks: int, host_blocks: int,
                  staging_slots: int = 1, copy_streams: int = 16, seed: int = 0,
                  device: str | torch.device = "cuda", record_timing: bool = False,
-                 fill: str = "random", prefetch_next: bool = True):
+                 fill: str = "random", prefetch_next: bool = True, binding: str = "ctypes"):
         if not torch.cuda.is_available():
             raise RuntimeError("B200Executor needs a CUDA device (there is no CPU fallback)")
         if staging_slots not in (1, 2):
@@ -92,7 +92,7 @@ class B200Executor:
         self.device = torch.device(device)
         self.pool = DevicePool(device_blocks, shape.num_kv_heads, self.device)
         self.host = HostArena(host_blocks, shape.block_bytes)
-        self.runtime = StepRuntime(copy_streams)
+        self.runtime = StepRuntime(copy_streams, binding=binding)
         self.staging_slots = staging_slots
         self.seed = seed
         self.fill = fill
@@ -458,7 +458,7 @@ class B200Executor:
         else:
             t0 = torch.cuda.Event(enable_timing=True)
             t0.record(stream)
-        self.runtime.decode_step(desc, stream)
+        self.runtime.decode_step(desc, stream, out=keep[1])
         t1.record(stream)
         self.steps += 1
         self.last_inputs, self.last_output = keep[0], keep[1]

@@ -19,17 +19,34 @@ def _ptr(a: np.ndarray) -> int:
 
 
 class StepRuntime:
-    """K2/K4 copy-engine orchestration + K1/K3 launches for whole steps."""
+    """K2/K4 copy-engine orchestration + K1/K3 launches for whole steps.
 
-    def __init__(self, max_copy_streams: int = 16):
+    ``binding`` picks how steps and migrations reach the library: ``"ctypes"``
+    (the C ABI directly) or ``"torch"`` (the dispatcher ops ``orbit::decode_step``
+    / ``orbit::migrate`` registered over the same ABI, ``torch_ops.py``)."""
+
+    def __init__(self, max_copy_streams: int = 16, binding: str = "ctypes"):
+        if binding not in ("ctypes", "torch"):
+            raise ValueError(f"unknown binding {binding!r}")
+        self.binding = binding
+        if binding == "torch":
+            from . import torch_ops
+
+            torch_ops.load()
         self.lib = _native.load()
         handle = self.lib.ofb_runtime_create(max_copy_streams)
         if not handle:
             raise _native.NativeError(f"ofb_runtime_create: {self.lib.ofb_last_error().decode()}")
         self.handle = handle
 
-    def decode_step(self, desc: _native.StepDesc, stream=None) -> None:
+    def decode_step(self, desc: _native.StepDesc, stream=None, out: torch.Tensor | None = None) -> None:
         s = stream if stream is not None else torch.cuda.current_stream()
+        if self.binding == "torch":
+            if out is None:
+                raise ValueError("the torch binding needs the step's output tensor")
+            with torch.cuda.stream(s):
+                torch.ops.orbit.decode_step(int(self.handle), ctypes.addressof(desc), out)
+            return
         rc = self.lib.ofb_runtime_decode_step(self.handle, ctypes.byref(desc), s.cuda_stream)
         _native.check(rc, "ofb_runtime_decode_step")
 
@@ -69,6 +86,14 @@ class StepRuntime:
         nbytes = np.ascontiguousarray(nbytes, dtype=np.int64)
         kinds = np.ascontiguousarray(kinds, dtype=np.int32)
         s = stream if stream is not None else torch.cuda.current_stream()
+        if self.binding == "torch":
+            anchor = torch.empty(0, device=s.device)
+            with torch.cuda.stream(s):
+                torch.ops.orbit.migrate(int(self.handle), torch.from_numpy(dst.view(np.int64)),
+                                        torch.from_numpy(src.view(np.int64)),
+                                        torch.from_numpy(nbytes), torch.from_numpy(kinds),
+                                        bool(record_timing), anchor)
+            return
         rc = self.lib.ofb_runtime_migrate(self.handle, n, _ptr(dst), _ptr(src), _ptr(nbytes),
                                           _ptr(kinds), int(record_timing), s.cuda_stream)
         _native.check(rc, "ofb_runtime_migrate")

@@ -27,15 +27,29 @@ def k1_variant(request):
     ops.set_attention_kernel(prev)
 
 
+_BINDING = ["ctypes"]
+
+
+@pytest.fixture(params=["ctypes", "torch"], autouse=True)
+def binding(request):
+    """...and through both bindings: the ctypes C ABI and torch.ops.orbit."""
+    _BINDING[0] = request.param
+    yield request.param
+    _BINDING[0] = "ctypes"
+
+
 def _run_gpu(case, max_seq_len=None):
-    from paper_2601_10729_b200 import ops
+    from paper_2601_10729_b200 import ops, torch_ops
 
     dev = torch.device("cuda:0")
-    out = ops.decode_attention(
-        case["q"].to(dev), case["pool"].to(dev),
-        torch.from_numpy(case["block_tables"]).to(dev),
-        torch.from_numpy(case["seq_lens"]).to(dev),
-        max_seq_len=max_seq_len, scale=case["scale"])
+    args = (case["q"].to(dev), case["pool"].to(dev),
+            torch.from_numpy(case["block_tables"]).to(dev),
+            torch.from_numpy(case["seq_lens"]).to(dev))
+    if _BINDING[0] == "torch":
+        msl = max_seq_len if max_seq_len is not None else int(case["seq_lens"].max(initial=0))
+        out = torch_ops.decode_attention(*args, msl, scale=case["scale"])
+    else:
+        out = ops.decode_attention(*args, max_seq_len=max_seq_len, scale=case["scale"])
     torch.cuda.synchronize()
     return out.float().cpu().numpy()
 
@@ -85,7 +99,7 @@ def test_empty_request_gives_zeros():
 
 @pytest.mark.parametrize("positions", [[4088, 17, 0, 300], [15, 16, 31, 47]])
 def test_append_bit_exact(positions):
-    from paper_2601_10729_b200 import ops
+    from paper_2601_10729_b200 import ops, torch_ops
 
     hkv, b = 2, len(positions)
     case = make_case([p + 1 for p in positions], 8, hkv, seed=5)
@@ -99,8 +113,9 @@ def test_append_bit_exact(positions):
 
     dev = torch.device("cuda:0")
     pool = case["pool"].to(dev)
-    ops.kv_append(k_new.to(dev), v_new.to(dev), pool, torch.from_numpy(case["block_tables"]).to(dev),
-                  torch.from_numpy(pos).to(dev))
+    append = torch_ops.kv_append if _BINDING[0] == "torch" else ops.kv_append
+    append(k_new.to(dev), v_new.to(dev), pool, torch.from_numpy(case["block_tables"]).to(dev),
+           torch.from_numpy(pos).to(dev))
     torch.cuda.synchronize()
     np.testing.assert_array_equal(bf16_bits(pool.cpu()), want)
 
