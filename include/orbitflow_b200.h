@@ -41,15 +41,28 @@ extern "C" {
 OFB_API const char* ofb_version(void);
 OFB_API const char* ofb_last_error(void);
 /* K1 work decomposition for later launches: 0 = persistent stream-K, 1 = fixed
- * splits + last-CTA combine, 2 = auto (default: the split kernel, which with its
- * current plan wins on every measured shape).  Returns the previous variant. */
+ * splits + last-CTA combine, 2 = auto (default: cluster for latency-bound
+ * launches, split otherwise), 3 = cluster splits combined through distributed
+ * shared memory.  Returns the previous variant. */
 OFB_API int ofb_set_attention_kernel(int32_t variant);
-/* Which decomposition a launch of this shape would use now: 0 stream-K, 1 split. */
+/* Which decomposition a launch of this shape would use now: 0 stream-K, 1 split,
+ * 3 cluster. */
 OFB_API int ofb_attention_variant_for(int32_t batch, int32_t num_kv_heads, int32_t max_seq_len);
 /* Split plan of the (default) split K1, host arithmetic only: blocks per split
  * and splits per (request, KV head) on a GPU with `num_sms` SMs and
  * `ctas_per_sm` resident K1 CTAs (ofb_device_info); the launch uses the same
  * function with the live device's values. */
+/* Cluster plan of the cluster K1 (host arithmetic): CTAs per cluster, clusters
+ * per (request, KV head), blocks per CTA and TMA ring depth, given
+ * cluster_slots[k] = clusters of 2^k CTAs the GPU places at once (k = 0..4,
+ * ofb_attention_cluster_slots).  Returns 1 when the shape is not a one-wave
+ * cluster shape (the cluster kernel refuses it; auto never picks it). */
+OFB_API int ofb_attention_cluster_plan(int32_t batch, int32_t num_kv_heads, int32_t max_seq_len,
+                                       const int32_t* cluster_slots, int32_t* cluster,
+                                       int32_t* clusters_per_pair, int32_t* blocks_per_cta,
+                                       int32_t* stages);
+/* cluster_slots[k] (k = 0..4) of this GPU for the cluster K1 (initialises the device). */
+OFB_API int ofb_attention_cluster_slots(int32_t* cluster_slots);
 OFB_API int ofb_attention_split_plan(int32_t batch, int32_t num_q_heads, int32_t num_kv_heads,
                                      int32_t max_seq_len, int32_t num_sms, int32_t ctas_per_sm,
                                      int32_t* blocks_per_split, int32_t* splits);
@@ -57,6 +70,11 @@ OFB_API int ofb_attention_split_plan(int32_t batch, int32_t num_q_heads, int32_t
  * past the dependency wait, first tile ready, last tile consumed, exit, SM id)
  * into `device_buffer` (uint64 [448][6]); NULL switches tracing off. */
 OFB_API int ofb_k1_trace(void* device_buffer);
+/* Same for any K1 variant with an explicit capacity in CTAs: the split kernel
+ * writes 8 stamps per CTA (entry, prologue done, first tile ready, ring drained,
+ * partial written, ticket taken, exit, SM id) at index
+ * (request * Hkv + kv head) * splits + split; CTAs past `ctas` are not traced. */
+OFB_API int ofb_k1_trace_sized(void* device_buffer, int32_t ctas);
 /* SM count and resident attention CTAs per SM on the current device. */
 OFB_API int ofb_device_info(int32_t* num_sms, int32_t* attn_ctas_per_sm);
 

@@ -100,7 +100,11 @@ SIGNATURES = {
     "ofb_last_error": (ctypes.c_char_p, []),
     "ofb_set_attention_kernel": (ctypes.c_int, [c_i32]),
     "ofb_k1_trace": (ctypes.c_int, [c_vp]),
+    "ofb_k1_trace_sized": (ctypes.c_int, [c_vp, c_i32]),
     "ofb_attention_variant_for": (ctypes.c_int, [c_i32, c_i32, c_i32]),
+    "ofb_attention_cluster_plan": (ctypes.c_int, [c_i32, c_i32, c_i32, ctypes.c_void_p, ctypes.c_void_p,
+                                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "ofb_attention_cluster_slots": (ctypes.c_int, [ctypes.c_void_p]),
     "ofb_attention_split_plan": (ctypes.c_int, [c_i32, c_i32, c_i32, c_i32, c_i32, c_i32,
                                                 ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)]),
     "ofb_device_info": (ctypes.c_int, [c_i32p, c_i32p]),

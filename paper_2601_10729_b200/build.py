@@ -19,7 +19,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_lib"
 LIB_NAME = "liborbitflow_b200.so"
-SOURCES = ["decode_attention.cu", "decode_attention_stream.cu", "kv_append.cu", "kv_prefill.cu", "runtime.cu",
+SOURCES = ["decode_attention.cu", "decode_attention_stream.cu", "decode_attention_cluster.cu", "kv_append.cu", "kv_prefill.cu", "runtime.cu",
            "oproj_allreduce.cu", "planner_gpu.cu",
            "planner.cpp"]
 

@@ -182,4 +182,55 @@ __device__ __forceinline__ float merged_value(const MergeSlots<kWarps>* ms, int 
   return acc / L;
 }
 
+// Two-phase merge of the CTA's warp states, used by the split and cluster
+// kernels: per-row weights once (g threads), then every (row, 4 dims) output
+// is a kWarps-term weighted sum of float4 smem loads - no per-element max /
+// exp2 / divide, which left the old per-element merge latency-bound (~2 us
+// with one 5-warp CTA per SM, tools/k1_split_trace.py).
+template <int kWarps>
+struct MergeWeights {
+  float w[kWarps][kMaxGroup];   // exp2(m_w - M) / L, 0 for a warp that saw no token
+  float lse[kMaxGroup];         // M + log2(L) (log2 domain), -inf for an empty row
+};
+
+template <int kWarps>
+__device__ __forceinline__ void merge_weights(const MergeSlots<kWarps>* ms, MergeWeights<kWarps>* mw,
+                                              int g, int tid) {
+  if (tid < g) {
+    const int row = tid;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) M = fmaxf(M, ms->m[w][row]);
+    float sc[kWarps];
+    float L = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const float mw_ = ms->m[w][row];
+      sc[w] = mw_ > -INFINITY ? fast_exp2(mw_ - M) : 0.f;
+      L += sc[w] * ms->l[w][row];
+    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) mw->w[w][row] = sc[w] * inv;
+    mw->lse[row] = L > 0.f ? M + __log2f(L) : -INFINITY;
+  }
+}
+
+// Normalised merged O of `row`, head dims 4q .. 4q+3.
+template <int kWarps>
+__device__ __forceinline__ float4 merged_quad(const MergeSlots<kWarps>* ms,
+                                              const MergeWeights<kWarps>* mw, int row, int q) {
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) {
+    const float wt = mw->w[w][row];
+    const float4 v = *reinterpret_cast<const float4*>(&ms->o[w][row][q * 4]);
+    acc.x += wt * v.x;
+    acc.y += wt * v.y;
+    acc.z += wt * v.z;
+    acc.w += wt * v.w;
+  }
+  return acc;
+}
+
 }  // namespace ofb

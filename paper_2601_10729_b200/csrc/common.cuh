@@ -113,6 +113,36 @@ __device__ __forceinline__ void pdl_trigger() {
 // Host: launch with programmatic stream serialization unless OFB_PDL=0.
 bool pdl_enabled();
 
+// ---------------------------------------------------------------- DSMEM
+// Address of `local` (this CTA's shared memory) in cluster CTA `rank`'s window.
+__device__ __forceinline__ uint32_t dsmem_map(const void* local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float dsmem_ld_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ float4 dsmem_ld_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr) : "memory");
+  return v;
+}
+
+// Ticket for a "last CTA to arrive" combine: one acq_rel atomic at gpu scope.
+// Called by one thread after a CTA barrier, its release half publishes every
+// write the CTA made before the barrier (release is cumulative over what
+// happens-before it) and its acquire half makes the other CTAs' published
+// partials visible to the winner - no separate __threadfence() round trips.
+__device__ __forceinline__ int ticket_acq_rel(int* p) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

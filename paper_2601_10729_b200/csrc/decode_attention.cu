@@ -47,16 +47,24 @@ struct AttnArgs {
   int blocks_per_split, max_splits;
   float scale_log2;
   int kv_ready;                 // 1: KV complete before the PDL wait (see the stream kernel)
+  unsigned long long* trace;    // diagnostics (ofb_k1_trace): kSplitTraceSlots stamps per CTA
+  int trace_ctas;               // capacity of `trace` in CTAs
 };
 
-struct MergeScratch {
-  float o[kConsumerWarps][kMaxGroup][kHeadDim + 4];
-  float m[kConsumerWarps][kMaxGroup];
-  float l[kConsumerWarps][kMaxGroup];
-};
+// split-kernel trace slots per CTA: entry, prologue done (table + seq_lens +
+// barriers), first tile ready, ring drained, partial written, ticket taken,
+// exit, SM id
+constexpr int kSplitTraceSlots = 8;
+
+__device__ __forceinline__ unsigned long long split_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 constexpr size_t kRingBytes = size_t(kStages) * kHeadBlockBytes;
-static_assert(sizeof(MergeScratch) <= kRingBytes, "merge scratch must fit in the ring");
+static_assert(sizeof(MergeSlots<kConsumerWarps>) + sizeof(MergeWeights<kConsumerWarps>) <= kRingBytes,
+              "merge scratch must fit in the ring");
 static_assert(kMaxGroup * kMaxSplits * sizeof(float) + kMaxGroup * 2 * sizeof(float) <= kRingBytes,
               "combine scratch must fit in the ring");
 
@@ -91,6 +99,17 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int lane = tid & 31;
+  unsigned long long* tr = nullptr;
+  if (a.trace) {
+    const int cta = (req * a.hkv + kvh) * gridDim.x + split;
+    if (cta < a.trace_ctas) tr = a.trace + (size_t)cta * kSplitTraceSlots;
+  }
+  if (tr && tid == 0) {
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    tr[0] = split_gtimer();
+    tr[7] = smid;
+  }
 
   // see decode_attention_stream.cu: the predecessor must be complete before q,
   // outputs or workspace are touched; with kv_ready (host-guaranteed) the
@@ -100,7 +119,9 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
   if (!early) pdl_wait();
   pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned, derived by an offset so the compiler keeps the shared space
+  // (shared loads / stores instead of generic ones)
+  uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + kRingBytes);
   uint64_t* empty = full + kStages;
   int32_t* blk_ids = reinterpret_cast<int32_t*>(empty + kStages);
@@ -125,9 +146,13 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
       for (int i = tid; i < g * kHeadDim; i += kAttnThreads)
         a.out[((size_t)req * a.hq + qh0) * kHeadDim + i] = __float2bfloat16(0.f);
     }
+    if (tr && tid == 0) tr[6] = split_gtimer();
     return;
   }
-  if (split >= nsplit) return;
+  if (split >= nsplit) {
+    if (tr && tid == 0) tr[6] = split_gtimer();
+    return;
+  }
   const int n = min(a.blocks_per_split, nblk - b_begin);
 
   if (tid == 0) {
@@ -139,6 +164,7 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
     fence_mbar_init();
   }
   __syncthreads();
+  if (tr && tid == 0) tr[1] = split_gtimer();
 
   const float NEG_INF = -INFINITY;
   // per-lane softmax state (rows r0 and r0+8 of the padded 16-row group)
@@ -186,6 +212,7 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
     for (int i = warp; i < n; i += kConsumerWarps) {
       const int st = i % kStages;
       mbar_wait(&full[st], (i / kStages) & 1);
+      if (tr && i == 0 && lane == 0) tr[2] = split_gtimer();
       const uint32_t base = smem_u32(ring + (size_t)st * kHeadBlockBytes);
       const int tok0 = (b_begin + i) * kBlockTokens;
       const bool partial = tok0 + kBlockTokens > seq;
@@ -279,17 +306,18 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
     l_run[1] += __shfl_xor_sync(0xffffffffu, l_run[1], 2);
   }
   __syncthreads();  // ring drained: every issued TMA was consumed
+  if (tr && tid == 0) tr[3] = split_gtimer();
 
   // -------------------------------------------------------- merge 4 warps
-  MergeScratch* ms = reinterpret_cast<MergeScratch*>(ring);
+  MergeSlots<kConsumerWarps>* ms = reinterpret_cast<MergeSlots<kConsumerWarps>*>(ring);
+  MergeWeights<kConsumerWarps>* mwt = reinterpret_cast<MergeWeights<kConsumerWarps>*>(
+      ring + sizeof(MergeSlots<kConsumerWarps>));
   if (warp < kConsumerWarps) {
 #pragma unroll
     for (int nt = 0; nt < 16; ++nt) {
       const int d = nt * 8 + c0;
-      ms->o[warp][r0][d] = o[nt][0];
-      ms->o[warp][r0][d + 1] = o[nt][1];
-      ms->o[warp][r0 + 8][d] = o[nt][2];
-      ms->o[warp][r0 + 8][d + 1] = o[nt][3];
+      *reinterpret_cast<float2*>(&ms->o[warp][r0][d]) = make_float2(o[nt][0], o[nt][1]);
+      *reinterpret_cast<float2*>(&ms->o[warp][r0 + 8][d]) = make_float2(o[nt][2], o[nt][3]);
     }
     if ((lane & 3) == 0) {
       ms->m[warp][r0] = m_run[0];
@@ -299,46 +327,44 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
     }
   }
   __syncthreads();
+  merge_weights<kConsumerWarps>(ms, mwt, g, tid);
+  __syncthreads();
 
   const bool single = (nsplit == 1);
-  for (int idx = tid; idx < g * kHeadDim; idx += kAttnThreads) {
-    const int row = idx / kHeadDim;
-    const int d = idx - row * kHeadDim;
-    float M = NEG_INF;
-#pragma unroll
-    for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, ms->m[w][row]);
-    float acc = 0.f, L = 0.f;
-#pragma unroll
-    for (int w = 0; w < kConsumerWarps; ++w) {
-      const float mw = ms->m[w][row];
-      if (mw != NEG_INF) {
-        const float sc = fast_exp2(mw - M);
-        acc += sc * ms->o[w][row][d];
-        L += sc * ms->l[w][row];
-      }
-    }
-    const float val = acc / L;
+  constexpr int kQ = kHeadDim / 4;
+  for (int it = tid; it < g * kQ; it += kAttnThreads) {
+    const int row = it / kQ;
+    const int q4 = it - row * kQ;
+    const float4 v = merged_quad<kConsumerWarps>(ms, mwt, row, q4);
     const size_t qrow = (size_t)req * a.hq + qh0 + row;
     if (single) {
-      a.out[qrow * kHeadDim + d] = __float2bfloat16(val);
+      __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(a.out + qrow * kHeadDim + q4 * 4);
+      dst[0] = __floats2bfloat162_rn(v.x, v.y);
+      dst[1] = __floats2bfloat162_rn(v.z, v.w);
     } else {
-      a.ws_o[(qrow * a.max_splits + split) * kHeadDim + d] = val;
-      if (d == 0) a.ws_lse[qrow * a.max_splits + split] = M + __log2f(L);
+      *reinterpret_cast<float4*>(a.ws_o + (qrow * a.max_splits + split) * kHeadDim + q4 * 4) = v;
+      if (q4 == 0) a.ws_lse[qrow * a.max_splits + split] = mwt->lse[row];
     }
   }
-  if (single) return;
+  if (tr && tid == 0) tr[4] = split_gtimer();
+  if (single) {
+    if (tr && tid == 0) tr[6] = split_gtimer();
+    return;
+  }
   if (early) pdl_wait();   // the producer warp joins the combine below
 
   // ------------------------------------------- last CTA combines the splits
   __syncthreads();        // every partial write of the CTA happens-before thread 0's
-  if (tid == 0) {         // gpu-scope fence + ticket (cumulative release)
-    __threadfence();
-    const int ticket = atomicAdd(&a.counters[req * a.hkv + kvh], 1);
+  if (tid == 0) {         // acq_rel ticket (cumulative release, acquire for the winner)
+    const int ticket = ticket_acq_rel(&a.counters[req * a.hkv + kvh]);
     *flag = (ticket == nsplit - 1);
   }
   __syncthreads();
-  if (!*flag) return;
-  __threadfence();
+  if (tr && tid == 0) tr[5] = split_gtimer();
+  if (!*flag) {
+    if (tr && tid == 0) tr[6] = split_gtimer();
+    return;
+  }
 
   float* wts = reinterpret_cast<float*>(ring);        // [16][nsplit]
   float* inv = wts + kMaxGroup * kMaxSplits;          // [16]
@@ -417,6 +443,7 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
     }
   }
   if (tid == 0) a.counters[req * a.hkv + kvh] = 0;  // re-arm for the next launch
+  if (tr && tid == 0) tr[6] = split_gtimer();
 }
 
 // ------------------------------------------------------------------ host side
@@ -506,6 +533,8 @@ static AttnPlan plan_splits(int batch, int hq, int hkv, int max_seq_len, int num
 }
 
 size_t attention_stream_workspace_bytes(int batch, int hq, int hkv, int max_seq_len);
+unsigned long long* k1_trace_buffer();
+int k1_trace_capacity();
 cudaError_t launch_decode_attention_stream(const CUtensorMap& map, const void* q, void* out,
                                            const int32_t* block_tables, int max_blocks,
                                            const int32_t* seq_lens, void* workspace,
@@ -513,30 +542,59 @@ cudaError_t launch_decode_attention_stream(const CUtensorMap& map, const void* q
                                            int max_seq_len, float scale, cudaStream_t stream,
                                            bool kv_ready);
 
-// K1 work decomposition: "stream" (persistent stream-K, default) or "split"
-// (fixed splits + last-CTA combine); OFB_K1=split selects the latter.
-bool stream_preferred(int batch, int hkv, int max_seq_len);
-
-// 0 = stream-K, 1 = fixed splits, 2 = auto (default; OFB_K1=stream|split pins one)
+// K1 work decomposition: 0 = persistent stream-K, 1 = fixed splits + last-CTA
+// combine, 3 = cluster splits with a DSMEM combine (decode_attention_cluster.cu),
+// 2 = auto (default; OFB_K1=stream|split|cluster pins one).
 static int g_k1_variant = -1;
 
 static int k1_variant() {
   if (g_k1_variant < 0) {
     const char* v = std::getenv("OFB_K1");
-    g_k1_variant = !v ? 2 : std::strcmp(v, "split") == 0 ? 1 : std::strcmp(v, "stream") == 0 ? 0 : 2;
+    g_k1_variant = !v ? 2
+                   : std::strcmp(v, "split") == 0   ? 1
+                   : std::strcmp(v, "stream") == 0  ? 0
+                   : std::strcmp(v, "cluster") == 0 ? 3
+                                                    : 2;
   }
   return g_k1_variant;
 }
 
-// Auto = split: with the split plan below (one CTA per SM, both slots only for
-// long splits) the split kernel beat stream-K on every shape of
-// profiles/r01_k1_sweep.md (B 1-32, 4K-64K, 8B / 70B / TP8-shard heads) and in
-// the cfg2 / cfg2r / cfg4 steps; stream-K stays selectable (variant 0).
-static bool use_split_kernel(int batch, int hkv, int max_seq_len) {
-  (void)batch;
-  (void)hkv;
-  (void)max_seq_len;
-  return k1_variant() != 0;
+size_t attention_cluster_workspace_bytes(int batch, int hq, int hkv, int max_seq_len);
+cudaError_t launch_decode_attention_cluster(const CUtensorMap& map, const void* q, void* out,
+                                            const int32_t* block_tables, int max_blocks,
+                                            const int32_t* seq_lens, void* workspace,
+                                            size_t workspace_bytes, int batch, int hq, int hkv,
+                                            int max_seq_len, float scale, cudaStream_t stream,
+                                            bool kv_ready);
+
+// Auto: the cluster kernel for latency-bound launches (the whole launch fits one
+// wave of one-CTA-per-SM clusters and moves little data), the split kernel
+// otherwise (with its plan it beat stream-K on every shape of
+// profiles/r01_k1_sweep.md); stream-K stays selectable (variant 0).
+int attention_cluster_slots(int* slots);
+int attention_cluster_plan(int batch, int hkv, int max_seq_len, const int* slots, int* C, int* P,
+                           int* bps, int* stages);
+
+// Fitted on tools/k1_variant_sweep.py (profiles/r02_k1_variants.md): the
+// cluster kernel wins when a pair gets a whole cluster and its CTAs stay short
+// (<= 4 (request, KV head) pairs, <= 40 blocks per CTA), and on tiny contexts
+// (<= 64 blocks) with <= 8 pairs; with more pairs the GPC packing of clusters
+// (7 x 16, 15 x 8, 33 x 4 CTAs on 148 SMs) leaves each pair too few CTAs.
+bool cluster_preferred(int batch, int hq, int hkv, int max_seq_len) {
+  (void)hq;
+  int slots[5], C, P, bps, stages;
+  if (attention_cluster_slots(slots) != 0) return false;
+  if (attention_cluster_plan(batch, hkv, max_seq_len, slots, &C, &P, &bps, &stages) != 0)
+    return false;
+  const long pairs = (long)batch * hkv;
+  const long nblk = (max_seq_len + kBlockTokens - 1) / kBlockTokens;
+  return (pairs <= 4 && bps <= 40) || (pairs <= 8 && nblk <= 64);
+}
+
+static int pick_variant(int batch, int hq, int hkv, int max_seq_len) {
+  const int v = k1_variant();
+  if (v != 2) return v;
+  return cluster_preferred(batch, hq, hkv, max_seq_len) ? 3 : 1;
 }
 
 bool pdl_enabled() {
@@ -561,13 +619,13 @@ int attention_split_plan(int batch, int hq, int hkv, int max_seq_len, int num_sm
   return 0;
 }
 
-int attention_variant_for(int batch, int hkv, int max_seq_len) {
-  return use_split_kernel(batch, hkv, max_seq_len) ? 1 : 0;
+int attention_variant_for(int batch, int hq, int hkv, int max_seq_len) {
+  return pick_variant(batch, hq, hkv, max_seq_len);
 }
 
 int set_attention_variant(int variant) {
   const int prev = k1_variant();
-  if (variant >= 0 && variant <= 2) g_k1_variant = variant;
+  if (variant >= 0 && variant <= 3) g_k1_variant = variant;
   return prev;
 }
 
@@ -576,7 +634,9 @@ static size_t split_workspace_bytes(int batch, int hq, int hkv, int max_seq_len)
 size_t attention_workspace_bytes(int batch, int hq, int hkv, int max_seq_len) {
   const size_t a = split_workspace_bytes(batch, hq, hkv, max_seq_len);
   const size_t b = attention_stream_workspace_bytes(batch, hq, hkv, max_seq_len);
-  return a > b ? a : b;
+  const size_t c = attention_cluster_workspace_bytes(batch, hq, hkv, max_seq_len);
+  const size_t ab = a > b ? a : b;
+  return ab > c ? ab : c;
 }
 
 static size_t split_workspace_bytes(int batch, int hq, int hkv, int max_seq_len) {
@@ -596,7 +656,12 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
                                     int max_seq_len, float scale, cudaStream_t stream,
                                     bool kv_ready) {
   if (batch <= 0) return cudaSuccess;
-  if (!use_split_kernel(batch, hkv, max_seq_len))
+  const int variant = pick_variant(batch, hq, hkv, max_seq_len);
+  if (variant == 3)
+    return launch_decode_attention_cluster(map, q, out, block_tables, max_blocks, seq_lens,
+                                           workspace, workspace_bytes, batch, hq, hkv,
+                                           max_seq_len, scale, stream, kv_ready);
+  if (variant == 0)
     return launch_decode_attention_stream(map, q, out, block_tables, max_blocks, seq_lens,
                                           workspace, workspace_bytes, batch, hq, hkv, max_seq_len,
                                           scale, stream, kv_ready);
@@ -631,6 +696,8 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
   a.max_splits = ws_splits;
   a.scale_log2 = scale * 1.4426950408889634f;
   a.kv_ready = kv_ready ? 1 : 0;
+  a.trace = k1_trace_buffer();
+  a.trace_ctas = a.trace ? k1_trace_capacity() : 0;
   dim3 grid(plan.max_splits, hkv, batch);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;

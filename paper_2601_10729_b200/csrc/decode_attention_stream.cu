@@ -338,8 +338,13 @@ paged_gqa_decode_stream_kernel(const __grid_constant__ CUtensorMap kv_map, const
 // ------------------------------------------------------------------ host side
 
 static unsigned long long* g_k1_trace = nullptr;
+static int g_k1_trace_ctas = 448;
 unsigned long long* k1_trace_buffer() { return g_k1_trace; }
-void set_k1_trace_buffer(void* buf) { g_k1_trace = static_cast<unsigned long long*>(buf); }
+int k1_trace_capacity() { return g_k1_trace_ctas; }
+void set_k1_trace_buffer(void* buf, int ctas) {
+  g_k1_trace = static_cast<unsigned long long*>(buf);
+  g_k1_trace_ctas = ctas > 0 ? ctas : 448;
+}
 
 static int g_stream_occ = 0, g_stream_sms = 0;
 

@@ -35,10 +35,13 @@ cudaError_t launch_kv_append(const void* k_new, const void* v_new, void* pool,
                              cudaStream_t stream);
 int attention_occupancy();
 int set_attention_variant(int variant);
-int attention_variant_for(int batch, int hkv, int max_seq_len);
+int attention_variant_for(int batch, int hq, int hkv, int max_seq_len);
+int attention_cluster_slots(int* slots);
+int attention_cluster_plan(int batch, int hkv, int max_seq_len, const int* slots, int* C, int* P,
+                           int* bps, int* stages);
 int attention_split_plan(int batch, int hq, int hkv, int max_seq_len, int num_sms, int occupancy,
                          int* blocks_per_split, int* splits);
-void set_k1_trace_buffer(void* buf);
+void set_k1_trace_buffer(void* buf, int ctas);
 cudaError_t launch_kv_prefill(const void* k, const void* v, const uint64_t* dst, int num_layers,
                               int tokens, int hkv, cudaStream_t stream);
 }  // namespace ofb
@@ -342,12 +345,33 @@ const char* ofb_version(void) { return "orbitflow-b200 0.1 sm_100a"; }
 const char* ofb_last_error(void) { return g_err.c_str(); }
 
 int ofb_set_attention_kernel(int32_t variant) {
-  if (variant < 0 || variant > 2) return fail(-1, "variant must be 0 (stream-K), 1 (split) or 2 (auto)");
+  if (variant < 0 || variant > 3)
+    return fail(-1, "variant must be 0 (stream-K), 1 (split), 2 (auto) or 3 (cluster)");
   return ofb::set_attention_variant(variant);
 }
 
 int ofb_attention_variant_for(int32_t batch, int32_t num_kv_heads, int32_t max_seq_len) {
-  return ofb::attention_variant_for(batch, num_kv_heads, max_seq_len);
+  return ofb::attention_variant_for(batch, num_kv_heads, num_kv_heads, max_seq_len);
+}
+
+int ofb_attention_cluster_plan(int32_t batch, int32_t num_kv_heads, int32_t max_seq_len,
+                               const int32_t* cluster_slots, int32_t* cluster,
+                               int32_t* clusters_per_pair, int32_t* blocks_per_cta,
+                               int32_t* stages) {
+  if (!cluster_slots || !cluster || !clusters_per_pair || !blocks_per_cta || !stages ||
+      max_seq_len < 0)
+    return ofb::report_error(-1, "ofb_attention_cluster_plan: bad arguments");
+  if (ofb::attention_cluster_plan(batch, num_kv_heads, max_seq_len, cluster_slots, cluster,
+                                  clusters_per_pair, blocks_per_cta, stages) != 0)
+    return ofb::report_error(1, "ofb_attention_cluster_plan: not a one-wave cluster shape");
+  return 0;
+}
+
+int ofb_attention_cluster_slots(int32_t* slots) {
+  if (!slots) return ofb::report_error(-1, "ofb_attention_cluster_slots: null pointer");
+  if (ofb::attention_cluster_slots(slots) != 0)
+    return ofb::report_error(1, "ofb_attention_cluster_slots: no device");
+  return 0;
 }
 
 int ofb_attention_split_plan(int32_t batch, int32_t num_q_heads, int32_t num_kv_heads,
@@ -360,7 +384,13 @@ int ofb_attention_split_plan(int32_t batch, int32_t num_q_heads, int32_t num_kv_
 }
 
 int ofb_k1_trace(void* device_buffer) {
-  ofb::set_k1_trace_buffer(device_buffer);
+  ofb::set_k1_trace_buffer(device_buffer, 448);
+  return 0;
+}
+
+int ofb_k1_trace_sized(void* device_buffer, int32_t ctas) {
+  if (ctas < 1) return fail(-1, "ofb_k1_trace_sized: capacity must be >= 1 CTA");
+  ofb::set_k1_trace_buffer(device_buffer, ctas);
   return 0;
 }
 

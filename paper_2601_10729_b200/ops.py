@@ -125,12 +125,26 @@ def device_info() -> tuple[int, int]:
 
 def set_attention_kernel(variant: str) -> str:
     """Select K1's work decomposition: "stream" (persistent stream-K), "split"
-    (fixed splits + last-CTA combine) or "auto" (default).  Returns the previous one."""
-    names = {"stream": 0, "split": 1, "auto": 2}
+    (fixed splits + last-CTA combine), "cluster" (cluster splits, DSMEM combine)
+    or "auto" (default).  Returns the previous one."""
+    names = {"stream": 0, "split": 1, "auto": 2, "cluster": 3}
     prev = _native.load().ofb_set_attention_kernel(names[variant])
     if prev < 0:
         _native.check(prev, "ofb_set_attention_kernel")
     return {v: k for k, v in names.items()}[prev]
+
+
+def cluster_plan(batch: int, hkv: int, max_seq_len: int) -> dict | None:
+    """The cluster K1's plan on this GPU (None: not a one-wave cluster shape)."""
+    lib = _native.load()
+    slots = (ctypes.c_int32 * 5)()
+    _native.check(lib.ofb_attention_cluster_slots(slots), "ofb_attention_cluster_slots")
+    out = [ctypes.c_int32() for _ in range(4)]
+    rc = lib.ofb_attention_cluster_plan(batch, hkv, max_seq_len, slots, *[ctypes.byref(o) for o in out])
+    if rc != 0:
+        return None
+    return {"cluster": out[0].value, "clusters_per_pair": out[1].value,
+            "blocks_per_cta": out[2].value, "stages": out[3].value, "slots": list(slots)}
 
 
 def kv_prefill(k: torch.Tensor, v: torch.Tensor, dst_addrs: torch.Tensor) -> None:

@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 RTOL, ATOL = 2e-2, 1e-2
 
 
-@pytest.fixture(params=["stream", "split"], autouse=True)
+@pytest.fixture(params=["stream", "split", "cluster"], autouse=True)
 def k1_variant(request):
     """Every K1 parity test runs under both work decompositions."""
     from paper_2601_10729_b200 import ops
