@@ -28,6 +28,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -184,10 +185,6 @@ __device__ __forceinline__ uint32_t map_to_cta(uint32_t saddr, uint32_t cta) {
   return r;
 }
 
-__device__ __forceinline__ void st_cluster_f32(uint32_t addr, float v) {
-  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
-}
-
 // Grid = tiles x splits, cluster = (splits, 1, 1): the CTAs of a cluster share
 // one hidden tile and split its K range; non-leaders ship their fp32 partial
 // into the leader's shared memory (DSMEM) and the leader sums in split order.
@@ -228,9 +225,10 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
-  // every CTA of the cluster has started before any DSMEM access (off the critical
-  // path: with PDL this prologue overlaps the previous kernel)
-  if (a.splits > 1) cluster_sync_all();
+  // "every CTA of the cluster has started" is only needed before the first DSMEM
+  // access: arrive now, wait right before the partials are shipped (by then every
+  // peer has long arrived, so the barrier is off the critical path)
+  if (a.splits > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   if (tr) tr[1] = globaltimer();
 
   if (warp == 0 && lane == 0) {
@@ -284,14 +282,19 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
   // bf16 in the ring (idle once the leader's own MMAs completed)
   float* red = reinterpret_cast<float*>(smem + static_cast<size_t>(a.stages) * stage_bytes);
   __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(smem);
+  if (a.splits > 1) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
   if (a.splits > 1 && split != 0) {
-    // ship this split's fp32 partial into the leader's smem
+    // ship this split's fp32 partial into the leader's smem: element (n, m) at
+    // n * 128 + m, so a warp's 32 rows are one contiguous 128-byte DSMEM store
     const uint32_t dst = map_to_cta(smem_u32(red + static_cast<size_t>(split - 1) * a.npad * kTileM), 0);
     for (int c = 0; c < a.npad / 32; ++c) {
       uint32_t v[32];
       tmem_ld32(trow + c * 32, v);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) st_cluster_f32(dst + ((c * 32 + j) * kTileM + m) * 4, __uint_as_float(v[j]));
+      for (int j = 0; j < 32; ++j)
+        asm volatile("st.shared::cluster.f32 [%0], %1;"
+                     ::"r"(dst + ((c * 32 + j) * kTileM + m) * 4), "f"(__uint_as_float(v[j]))
+                     : "memory");
     }
     tc_fence_before();
     __syncthreads();
@@ -501,6 +504,35 @@ int get_maps(const ofb_oproj_desc* d, int npad, CUtensorMap* xmap, CUtensorMap* 
   return 0;
 }
 
+// Clusters of this launch's shape the GPU holds at once (cached per device,
+// cluster size and dynamic smem).
+int oproj_coresident_clusters(const cudaLaunchConfig_t* launch, const cudaLaunchAttribute* cluster_attr,
+                              int* out) {
+  static std::mutex mu;
+  static std::vector<std::array<long long, 4>> cache;   // dev, splits, smem, clusters
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return report_cuda(e, "cudaGetDevice");
+  const long long key_splits = cluster_attr->val.clusterDim.x;
+  const long long key_smem = static_cast<long long>(launch->dynamicSmemBytes);
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto& c : cache)
+    if (c[0] == dev && c[1] == key_splits && c[2] == key_smem) {
+      *out = static_cast<int>(c[3]);
+      return 0;
+    }
+  cudaLaunchConfig_t cfg = *launch;
+  cudaLaunchAttribute attr = *cluster_attr;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  e = cudaOccupancyMaxActiveClusters(&n, oproj_allreduce_kernel, &cfg);
+  if (e != cudaSuccess) return report_cuda(e, "cudaOccupancyMaxActiveClusters(oproj_allreduce_kernel)");
+  cache.push_back({dev, key_splits, key_smem, n});
+  *out = n;
+  return 0;
+}
+
 }  // namespace
 }  // namespace ofb
 
@@ -643,6 +675,22 @@ int ofb_oproj_allreduce(const ofb_oproj_desc* d, void* stream) {
   attr[0].val.clusterDim.x = splits;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  if (d->world > 1) {
+    // Forward progress of the exchange: a tile's CTA spins until every rank's
+    // copy of that tile has landed, so all tiles of every rank must be resident
+    // at once (any CTA still waiting for an SM could be the one a spinning peer
+    // needs).  Refuse a grid larger than what the GPU co-schedules.
+    int coresident = 0;
+    rc = oproj_coresident_clusters(&cfg, attr, &coresident);
+    if (rc) return rc;
+    if (tiles > coresident)
+      return report_error(-1, ("ofb_oproj_allreduce: " + std::to_string(tiles) + " clusters of " +
+                               std::to_string(splits) + " CTAs exceed the " +
+                               std::to_string(coresident) +
+                               " this GPU co-schedules; the peer-flag wait needs the whole grid "
+                               "resident (use hidden <= 128 x that many tiles, or world 1)")
+                                  .c_str());
+  }
   // W_o prefetch overlaps the attention kernel's tail (the x loads wait)
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;

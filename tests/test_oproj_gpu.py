@@ -110,6 +110,32 @@ def test_missing_peer_times_out_and_is_reported():
         bufs[0].close()
 
 
+def test_exchange_refuses_a_grid_the_gpu_cannot_hold_at_once():
+    """Every tile's CTA spins on its peers' flags, so the exchange is only safe
+    when the whole grid is co-resident: a launch with more tiles than the GPU
+    co-schedules (here 200 hidden tiles of one CTA each, > 148 SMs at one
+    200 KiB CTA per SM) is refused before anything runs, while the same shape
+    without an exchange (world 1) still launches."""
+    from paper_2601_10729_b200.collective import OprojAllReduce, SymmetricBuffers
+
+    dev = torch.device("cuda:0")
+    b, k, h = 8, 128, 128 * 200
+    bufs = SymmetricBuffers.emulated(2, b, h, device=dev)
+    try:
+        xs, ws = _inputs(2, 1, b, k, h, seed=9)
+        op = OprojAllReduce(ws[0].to(dev), b, bufs[0])
+        with pytest.raises(RuntimeError, match="co-schedules"):
+            op(xs[0].to(dev), 0)
+        torch.cuda.synchronize()
+        single = OprojAllReduce(ws[0].to(dev), b)
+        out = single(xs[0].to(dev), 0)
+        torch.cuda.synchronize()
+        want = xs[0][0].float() @ ws[0][0].float().T
+        torch.testing.assert_close(out.float().cpu(), want, rtol=RTOL, atol=ATOL)
+    finally:
+        bufs[0].close()
+
+
 def _ipc_worker(rank, world, port, b, k, h, q):
     import torch.distributed as dist
 
