@@ -879,7 +879,34 @@ def run_cfg3_policies(args):
                       "policies": rows}), flush=True)
 
 
+def _recording_executor(base_cls):
+    """The executor with per-step algorithmic bytes recorded:
+    HOST = blocks_to_fetch x block bytes (src/latency.py:99-105), HBM = the
+    resident layers' KV of every request + q / out + the appended token."""
+    from paper_2601_10729_b200.latency import blocks_to_fetch
+
+    class Recording(base_cls):
+        def decode_step(self, batch, placement=None, inputs=None, sync=True):
+            ms = super().decode_step(batch, placement, inputs, sync=sync)
+            shape = self.shape
+            host = blocks_to_fetch(placement, batch) * shape.block_bytes
+            hbm = sum(row.count(1) * (r.total_tokens + 1) for r, row in zip(batch, placement.rows)) \
+                * shape.kv_bytes_per_token
+            hbm += len(batch) * shape.num_layers * (2 * shape.num_q_heads * 128 * 2
+                                                     + shape.kv_bytes_per_token)
+            self.step_bytes.append((len(batch), host, hbm))
+            return ms
+
+    return Recording
+
+
 def run_cfg3(args):
+    """Config 3 through the serving engine in all three clock modes, side by side:
+    parity (model time; decisions must equal the executor-less run), live (the
+    measured device step drives the clock) and live-wall (host wall time: solve,
+    install, Python and the device step).  Per mode: tokens/s, TPOT / TBT
+    attainment, the batch-size histogram, per-step HOST / HBM algorithmic bytes
+    against the binding roofline, and host-control ms per step."""
     import torch
 
     from paper_2601_10729_b200.engine import Simulation
@@ -888,6 +915,9 @@ def run_cfg3(args):
     from paper_2601_10729_b200.policies import PolicyKind, make_policy
 
     trace, profile, slo, cfg = cfg3_setup(args)
+    peaks = _measured_peaks()
+    hbm_peak = float(peaks.get("hbm_gbs", 6450.0))
+    h2d_peak, _d2h = _probe_link(torch.device("cuda"))
 
     def simulate(executor, mode):
         policy = make_policy(PolicyKind.ORBIT, profile, slo, max_batch=cfg.max_batch,
@@ -900,35 +930,69 @@ def run_cfg3(args):
     model_log, model_s = simulate(None, "parity")
     out = {"metric": METRIC, "config": "cfg3",
            "workload": "Llama-3.1-8B shape, mixed 8K-128K lognormal trace (seed 3), OrbitPolicy, "
-                       f"max_batch 4, HBM budget {profile.gpu_block_budget} blocks x 64 KiB",
+                       f"max_batch 4, HBM budget {profile.gpu_block_budget} blocks x 64 KiB "
+                       f"({profile.gpu_block_budget * 65536 / 2**30:.1f} GiB)",
            "requests": len(trace.requests),
            "prompts": [r.prompt_tokens for r in trace.requests],
            "profile": {"source": "measured on this GPU" if args.cfg3_calibrate
                        else "round-1 B200 constants (calibrate.py)",
                        "compute_base_ms": profile.compute_base_ms,
                        "compute_per_token_ms": profile.compute_per_token_ms,
-                       "bandwidth_blocks_per_ms": profile.bandwidth_blocks_per_ms}}
+                       "bandwidth_blocks_per_ms": profile.bandwidth_blocks_per_ms},
+           "peaks": {"hbm_gbs": hbm_peak, "h2d_gbs": h2d_peak}}
     steps_model = [r for r in model_log if r["kind"] == "step"]
-    out["host_control_ms_per_step"] = model_s * 1e3 / max(1, len(steps_model))
-    for mode in ("parity", "live"):
-        ex = B200Executor.for_trace(trace, profile, shape=LLAMA31_8B, max_batch=cfg.max_batch)
-        log, wall_s = simulate(ex, mode)
+    out["model_host_control_ms_per_step"] = model_s * 1e3 / max(1, len(steps_model))
+    recording = _recording_executor(B200Executor)
+    for mode in ("parity", "live", "live-wall"):
+        ex = recording.for_trace(trace, profile, shape=LLAMA31_8B, max_batch=cfg.max_batch)
+        ex.step_bytes = []
+        with ClockSampler(0) as clocks:
+            log, wall_s = simulate(ex, mode)
         steps = [r for r in log if r["kind"] == "step"]
-        gpu_ms = sum(r["payload"]["measured_us"] for r in steps) / 1e3
+        gpu = [r["payload"]["measured_us"] / 1e3 for r in steps]
+        gpu_ms = sum(gpu)
         tokens = sum(len(r["payload"]["ids"]) for r in steps)
         rep = collect_metrics(log)
+        hist = {}
+        for b, _h, _m in ex.step_bytes:
+            hist[b] = hist.get(b, 0) + 1
+        roof = [max(m / (hbm_peak * 1e9), h / (h2d_peak * 1e9)) * 1e3 for _b, h, m in ex.step_bytes]
+        link_bound = sum(1 for _b, h, m in ex.step_bytes if h / h2d_peak > m / hbm_peak)
+        host = sum(h for _b, h, _m in ex.step_bytes)
+        hbm = sum(m for _b, _h, m in ex.step_bytes)
         rec = {"steps": len(steps), "tokens": tokens, "gpu_ms": gpu_ms,
                "tokens_per_s_gpu": tokens / (gpu_ms * 1e-3), "wall_s": wall_s,
                "tpot_attainment": rep.tpot_attainment, "tbt_attainment": rep.tbt_attainment,
-               "tbt_p95_ms": rep.tbt_p95_ms, "pauses": rep.pauses, "resumes": rep.resumes,
-               "replans": rep.replans, "migrated": dict(ex.migrated),
-               "prefetch": ex.runtime.prefetch_stats()}
+               "tpot_p95_ms": rep.tpot_p95_ms, "tbt_p95_ms": rep.tbt_p95_ms,
+               "batch_histogram": dict(sorted(hist.items())),
+               "mean_batch": tokens / max(1, len(steps)),
+               "pauses": rep.pauses, "resumes": rep.resumes, "replans": rep.replans,
+               "preemptions": rep.preemptions, "migrated": dict(ex.migrated),
+               "prefetch": ex.runtime.prefetch_stats(),
+               "step_roofline": {
+                   "host_alg_bytes_total": host, "hbm_alg_bytes_total": hbm,
+                   "host_link_bound_steps": link_bound, "hbm_bound_steps": len(roof) - link_bound,
+                   "host_gbs_over_gpu_time": host / (gpu_ms * 1e-3) / 1e9,
+                   "hbm_gbs_over_gpu_time": hbm / (gpu_ms * 1e-3) / 1e9,
+                   "roofline_ms_total": sum(roof), "measured_ms_total": gpu_ms,
+                   "achieved_frac": sum(roof) / gpu_ms if gpu_ms else None,
+                   "per_step_first8": [{"B": b, "host_bytes": h, "hbm_bytes": m,
+                                        "roofline_ms": rf, "measured_ms": g}
+                                       for (b, h, m), rf, g in list(zip(ex.step_bytes, roof, gpu))[:8]]},
+               "clocks": clocks.summary()}
+        if mode == "live-wall":
+            walls = [r["payload"]["wall_us"] / 1e3 for r in steps if "wall_us" in r["payload"]]
+            rec["host_control_ms_per_step_median"] = statistics.median(
+                w - g for w, g in zip(walls, gpu)) if walls else None
+            rec["tokens_per_s_clock"] = tokens / (sum(walls) * 1e-3) if walls else None
         if mode == "parity":
             stripped = [dict(r, payload={k: v for k, v in r["payload"].items() if k != "measured_us"})
                         if r["kind"] == "step" else r for r in log]
             rec["decisions_match_model_run"] = stripped == model_log
             rec["model_tpot_attainment"] = collect_metrics(model_log).tpot_attainment
         out[mode] = rec
+        print(json.dumps({"mode": mode, **{k: v for k, v in rec.items()
+                                            if k not in ("step_roofline",)}}), file=sys.stderr, flush=True)
         ex.close()
         torch.cuda.synchronize()
     print(json.dumps(out), flush=True)
@@ -1106,9 +1170,10 @@ def main():
                                                            "cfg5"],
                     default="cfg2")
     ap.add_argument("--slo-scale", type=float, default=1.5)
-    ap.add_argument("--cfg3-requests", type=int, default=10)
+    ap.add_argument("--cfg3-requests", type=int, default=24)
     ap.add_argument("--cfg3-output-median", type=int, default=48)
-    ap.add_argument("--cfg3-budget-blocks", type=int, default=100000)
+    ap.add_argument("--cfg3-budget-blocks", type=int, default=655360,
+                    help="cfg3 HBM pool in 64 KiB blocks (SURVEY.md 8(d): a 40 GiB pool)")
     ap.add_argument("--cfg3-calibrate", action="store_true",
                     help="cfg3: SystemProfile measured on this GPU (K1 slope/intercept, link)")
     ap.add_argument("--cfg3-policies", default="",

@@ -1,4 +1,7 @@
-// K1, persistent stream-K decomposition (default).
+// K1, persistent stream-K decomposition (variant 0; selectable, not the
+// default: the split kernel - and the cluster kernel on latency-bound shapes -
+// measured faster on every shape of profiles/r01_k1_sweep.md and
+// profiles/r02_k1_variants.md).
 //
 // Same arithmetic as decode_attention.cu (attn_tile.cuh), different work
 // split: all (request, kv head, block) tiles of the layer are flattened into
