@@ -296,9 +296,26 @@ typedef struct ofb_oproj_desc {
   int32_t w_layout;    /* 0: w is [layers][hidden][k] (Linear); 1: packed
                           [layers][hidden/128][k/64][128][64] - every TMA box a
                           contiguous 16 KiB (weights are static: pack once) */
+  const void* residual; /* NULL, or bf16 [batch][hidden] added to the reduced sum before
+                          the single rounding (the decoder's x += o_proj(attn)); may
+                          alias `out`, identical on every rank */
+  int32_t out_parts;    /* 0/1: `out` is [batch][hidden].  n in 2..4 (world 1 only): the
+                          hidden columns are cut into n consecutive ranges of
+                          part_cols[i] (multiples of 128) written to separate bf16
+                          [batch][part_cols[i]] tensors part_out[i] - e.g. one launch for
+                          the q / k / v projections straight into their own buffers */
+  int32_t part_cols[4];
+  void* part_out[4];
 } ofb_oproj_desc;
 
 OFB_API int ofb_oproj_allreduce(const ofb_oproj_desc* desc, void* stream);
+
+/* ---- decoder glue of the whole-decoder TP step (cfg4; not a north-star piece) */
+/* out[r] = x[r] / sqrt(mean(x[r]^2) + eps) * weight, bf16 [rows][hidden], hidden % 8 == 0. */
+OFB_API int ofb_rmsnorm(const void* x, const void* weight, void* out, int32_t rows, int32_t hidden,
+                        float eps, void* stream);
+/* act[b][i] = silu(gate_up[b][i]) * gate_up[b][inter + i], bf16, inter % 8 == 0. */
+OFB_API int ofb_silu_mul(const void* gate_up, void* act, int32_t batch, int32_t inter, void* stream);
 /* Diagnostics: K6 launches write globaltimer stamps per CTA (entry, prologue done,
  * accumulator ready, cluster synced, output start, exit) into `device_buffer`
  * (uint64 [grid][8]); NULL switches tracing off. */

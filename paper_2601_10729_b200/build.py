@@ -20,7 +20,7 @@ CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_lib"
 LIB_NAME = "liborbitflow_b200.so"
 SOURCES = ["decode_attention.cu", "decode_attention_stream.cu", "decode_attention_cluster.cu", "kv_append.cu", "kv_prefill.cu", "runtime.cu",
-           "oproj_allreduce.cu", "planner_gpu.cu",
+           "oproj_allreduce.cu", "decoder_glue.cu", "planner_gpu.cu",
            "planner.cpp"]
 
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -183,9 +183,12 @@ class OprojAllReduce:
                                                                          device=self.w.device)
 
     def __call__(self, x: torch.Tensor, layer: int, out: torch.Tensor | None = None,
-                 stream=None) -> torch.Tensor:
+                 stream=None, residual: torch.Tensor | None = None,
+                 parts: list | None = None) -> torch.Tensor:
         """``x``: bf16 [L, B, K] (or [L, B, Hq_local, 128]) - all layers' attention
-        output; layer ``layer`` is projected.  Returns bf16 [B, H]."""
+        output; layer ``layer`` is projected.  Returns bf16 [B, H].  ``residual``
+        (bf16 [B, H], may be ``out`` itself) is added before the one rounding:
+        the decoder's ``x += o_proj(attn)`` in the same kernel."""
         if not x.is_cuda or x.dtype != torch.bfloat16:
             raise ValueError("x must be a bf16 CUDA tensor (no CPU fallback)")
         if x.shape[0] != self.layers:
@@ -194,19 +197,41 @@ class OprojAllReduce:
         x = x.reshape(self.layers, b, -1)
         if x.shape[2] != self.k or not x.is_contiguous():
             raise ValueError(f"x must be contiguous [layers, batch, {self.k}]")
-        if out is None:
+        if parts is not None:     # column ranges into separate [B, cols] tensors (world 1)
+            if out is not None or residual is not None or not 2 <= len(parts) <= 4:
+                raise ValueError("parts excludes out / residual and takes 2-4 tensors")
+            if self.symm is not None and self.symm.world > 1:
+                raise ValueError("parts is a single-rank projection (column-parallel)")
+            if sum(t.shape[-1] for t in parts) != self.hidden:
+                raise ValueError("the parts' columns must add up to hidden")
+            for t in parts:
+                if (t.dtype != torch.bfloat16 or not t.is_contiguous() or t.device != x.device
+                        or t.reshape(b, -1).shape[1] % 128):
+                    raise ValueError("parts must be contiguous bf16 [B, cols] tensors, cols % 128 == 0")
+        if out is None and parts is None:
             out = torch.empty((b, self.hidden), dtype=torch.bfloat16, device=x.device)
-        elif (out.shape != (b, self.hidden) or out.dtype != torch.bfloat16 or not out.is_contiguous()
+        elif out is not None and (out.shape != (b, self.hidden) or out.dtype != torch.bfloat16 or not out.is_contiguous()
               or out.device != x.device):
             raise ValueError(f"out must be a contiguous bf16 [{b}, {self.hidden}] tensor on {x.device}")
         d = _native.OprojDesc()
-        d.x, d.w, d.out = x.data_ptr(), self.w.data_ptr(), out.data_ptr()
+        d.x, d.w = x.data_ptr(), self.w.data_ptr()
+        d.out = out.data_ptr() if out is not None else None
+        if parts is not None:
+            d.out_parts = len(parts)
+            for i, t in enumerate(parts):
+                d.part_cols[i] = t.reshape(b, -1).shape[1]
+                d.part_out[i] = t.data_ptr()
         d.layers, d.layer, d.batch, d.k, d.hidden = self.layers, layer, b, self.k, self.hidden
         d.workspace, d.workspace_bytes = self.ws.data_ptr(), self.ws.numel()
         d.max_batch = self.max_batch
         d.status = self._status.data_ptr()
         d.timeout_ns = self.timeout_ns
         d.w_layout = self.w_layout
+        if residual is not None:
+            if (residual.shape != out.shape or residual.dtype != torch.bfloat16
+                    or not residual.is_contiguous() or residual.device != x.device):
+                raise ValueError(f"residual must be a contiguous bf16 [{b}, {self.hidden}] tensor")
+            d.residual = residual.data_ptr()
         if self.symm is None or self.symm.world == 1:
             d.world, d.rank, d.epoch = 1, 0, 1
             if self.symm is not None:
@@ -219,4 +244,4 @@ class OprojAllReduce:
         s = stream if stream is not None else torch.cuda.current_stream(x.device)
         _check(_lib().ofb_oproj_allreduce(ctypes.byref(d), ctypes.c_void_p(s.cuda_stream)),
                "ofb_oproj_allreduce")
-        return out
+        return out if parts is None else parts

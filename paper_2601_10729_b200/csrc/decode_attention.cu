@@ -24,9 +24,15 @@
 
 namespace ofb {
 
+// Two instantiations: narrow (4 consumer warps, 8-stage ring, two CTAs per SM)
+// for bandwidth-bound launches, wide (8 consumer warps, 16 stages, one CTA per
+// SM) for launches whose whole grid is one wave: there a CTA's own tile rate
+// bounds the launch, and a second warp per scheduler hides the tile latency.
 constexpr int kConsumerWarps = 4;
 constexpr int kAttnThreads = (kConsumerWarps + 1) * 32;
 constexpr int kStages = 8;
+constexpr int kWideWarps = 8;
+constexpr int kWideStages = 16;
 constexpr int kMaxSplits = 256;
 constexpr int kMaxBlocksPerSplit = 256;
 // Split tickets live in a fixed region at the start of the workspace, sized for
@@ -68,6 +74,16 @@ static_assert(sizeof(MergeSlots<kConsumerWarps>) + sizeof(MergeWeights<kConsumer
 static_assert(kMaxGroup * kMaxSplits * sizeof(float) + kMaxGroup * 2 * sizeof(float) <= kRingBytes,
               "combine scratch must fit in the ring");
 
+static_assert(sizeof(MergeSlots<kWideWarps>) + sizeof(MergeWeights<kWideWarps>) <=
+                  size_t(kWideStages) * kHeadBlockBytes,
+              "wide merge scratch must fit in the wide ring");
+
+template <int kW, int kS>
+constexpr size_t attn_smem_bytes() {
+  return 1024 + size_t(kS) * kHeadBlockBytes + 2 * kS * sizeof(uint64_t) +
+         kMaxBlocksPerSplit * sizeof(int32_t) + 16;
+}
+
 constexpr size_t kAttnSmemBytes = 1024 /*align slack*/ + kRingBytes +
                                   2 * kStages * sizeof(uint64_t) +
                                   kMaxBlocksPerSplit * sizeof(int32_t) + 16;
@@ -91,8 +107,10 @@ __device__ __forceinline__ void combine_round(float4& acc, const float4* __restr
   }
 }
 
-__global__ void __launch_bounds__(kAttnThreads, 2)
-paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnArgs a) {
+template <int kW, int kS>
+__device__ __forceinline__ void paged_gqa_decode_body(const CUtensorMap& kv_map, const AttnArgs& a) {
+  constexpr int kThr = (kW + 1) * 32;
+  constexpr size_t kRing = size_t(kS) * kHeadBlockBytes;
   const int split = blockIdx.x;
   const int kvh = blockIdx.y;
   const int req = blockIdx.z;
@@ -122,9 +140,9 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
   // 1024-aligned, derived by an offset so the compiler keeps the shared space
   // (shared loads / stores instead of generic ones)
   uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kRingBytes);
-  uint64_t* empty = full + kStages;
-  int32_t* blk_ids = reinterpret_cast<int32_t*>(empty + kStages);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kRing);
+  uint64_t* empty = full + kS;
+  int32_t* blk_ids = reinterpret_cast<int32_t*>(empty + kS);
   int* flag = blk_ids + kMaxBlocksPerSplit;
   // The split's table run is loaded speculatively (bounded by the row, not by
   // the sequence length) so it does not wait for the seq_lens round trip.
@@ -132,7 +150,7 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
   {
     const int span = min(a.blocks_per_split, a.max_blocks - b_begin);
     const int32_t* bt = a.block_tables + (size_t)req * a.max_blocks + b_begin;
-    for (int i = tid; i < span; i += kAttnThreads) blk_ids[i] = bt[i];
+    for (int i = tid; i < span; i += kThr) blk_ids[i] = bt[i];
   }
   const int seq = a.seq_lens[req];
   const int nblk = (seq + kBlockTokens - 1) / kBlockTokens;
@@ -143,7 +161,7 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
   if (nblk == 0) {  // empty request: defined output
     if (early) pdl_wait();
     if (split == 0) {
-      for (int i = tid; i < g * kHeadDim; i += kAttnThreads)
+      for (int i = tid; i < g * kHeadDim; i += kThr)
         a.out[((size_t)req * a.hq + qh0) * kHeadDim + i] = __float2bfloat16(0.f);
     }
     if (tr && tid == 0) tr[6] = split_gtimer();
@@ -157,7 +175,7 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
 
   if (tid == 0) {
     prefetch_tma_desc(&kv_map);
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -174,12 +192,12 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
   const int r0 = lane >> 2;
   const int c0 = (lane & 3) * 2;
 
-  if (warp == kConsumerWarps) {
+  if (warp == kW) {
     // ---------------------------------------------------------- producer
     if (lane == 0) {
       for (int i = 0; i < n; ++i) {
-        const int st = i % kStages;
-        if (i >= kStages) mbar_wait(&empty[st], ((i / kStages) - 1) & 1);
+        const int st = i % kS;
+        if (i >= kS) mbar_wait(&empty[st], ((i / kS) - 1) & 1);
         const int row = (blk_ids[i] * a.hkv + kvh) * kTileRows;
         uint8_t* dst = ring + (size_t)st * kHeadBlockBytes;
         mbar_arrive_expect_tx(&full[st], kHeadBlockBytes);
@@ -209,9 +227,9 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
 
     const int mi = lane >> 3;  // ldmatrix sub-matrix this lane addresses
     const int mr = lane & 7;
-    for (int i = warp; i < n; i += kConsumerWarps) {
-      const int st = i % kStages;
-      mbar_wait(&full[st], (i / kStages) & 1);
+    for (int i = warp; i < n; i += kW) {
+      const int st = i % kS;
+      mbar_wait(&full[st], (i / kS) & 1);
       if (tr && i == 0 && lane == 0) tr[2] = split_gtimer();
       const uint32_t base = smem_u32(ring + (size_t)st * kHeadBlockBytes);
       const int tok0 = (b_begin + i) * kBlockTokens;
@@ -309,10 +327,10 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
   if (tr && tid == 0) tr[3] = split_gtimer();
 
   // -------------------------------------------------------- merge 4 warps
-  MergeSlots<kConsumerWarps>* ms = reinterpret_cast<MergeSlots<kConsumerWarps>*>(ring);
-  MergeWeights<kConsumerWarps>* mwt = reinterpret_cast<MergeWeights<kConsumerWarps>*>(
-      ring + sizeof(MergeSlots<kConsumerWarps>));
-  if (warp < kConsumerWarps) {
+  MergeSlots<kW>* ms = reinterpret_cast<MergeSlots<kW>*>(ring);
+  MergeWeights<kW>* mwt = reinterpret_cast<MergeWeights<kW>*>(
+      ring + sizeof(MergeSlots<kW>));
+  if (warp < kW) {
 #pragma unroll
     for (int nt = 0; nt < 16; ++nt) {
       const int d = nt * 8 + c0;
@@ -327,15 +345,15 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
     }
   }
   __syncthreads();
-  merge_weights<kConsumerWarps>(ms, mwt, g, tid);
+  merge_weights<kW>(ms, mwt, g, tid);
   __syncthreads();
 
   const bool single = (nsplit == 1);
   constexpr int kQ = kHeadDim / 4;
-  for (int it = tid; it < g * kQ; it += kAttnThreads) {
+  for (int it = tid; it < g * kQ; it += kThr) {
     const int row = it / kQ;
     const int q4 = it - row * kQ;
-    const float4 v = merged_quad<kConsumerWarps>(ms, mwt, row, q4);
+    const float4 v = merged_quad<kW>(ms, mwt, row, q4);
     const size_t qrow = (size_t)req * a.hq + qh0 + row;
     if (single) {
       __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(a.out + qrow * kHeadDim + q4 * 4);
@@ -368,7 +386,7 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
 
   float* wts = reinterpret_cast<float*>(ring);        // [16][nsplit]
   float* inv = wts + kMaxGroup * kMaxSplits;          // [16]
-  for (int row = warp; row < g; row += kAttnThreads / 32) {
+  for (int row = warp; row < g; row += kThr / 32) {
     const size_t qrow = (size_t)req * a.hq + qh0 + row;
     float M = NEG_INF;
     for (int s2 = lane; s2 < nsplit; s2 += 32) {
@@ -396,9 +414,9 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
   // meet in smem.
   constexpr int kQuads = kHeadDim / 4;
   const int items = g * kQuads;
-  const int parts = items >= kAttnThreads ? 1 : kAttnThreads / items;
+  const int parts = items >= kThr ? 1 : kThr / items;
   float4* red = reinterpret_cast<float4*>(inv + kMaxGroup);   // [parts][items]
-  for (int it = tid; it < items * parts; it += kAttnThreads) {
+  for (int it = tid; it < items * parts; it += kThr) {
     const int item = it % items;
     const int part = it / items;
     const int row = item / kQuads;
@@ -424,7 +442,7 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
   }
   if (parts > 1) {
     __syncthreads();
-    for (int item = tid; item < items; item += kAttnThreads) {
+    for (int item = tid; item < items; item += kThr) {
       float4 acc = red[item];
       for (int p = 1; p < parts; ++p) {
         const float4 v = red[p * items + item];
@@ -446,6 +464,19 @@ paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnAr
   if (tr && tid == 0) tr[6] = split_gtimer();
 }
 
+// The two instantiations, each with its own launch bounds (narrow: two CTAs per SM).
+__global__ void __launch_bounds__(160, 2)
+paged_gqa_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnArgs a) {
+  paged_gqa_decode_body<kConsumerWarps, kStages>(kv_map, a);
+}
+
+__global__ void __launch_bounds__(288, 1)
+paged_gqa_decode_wide_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnArgs a) {
+  paged_gqa_decode_body<kWideWarps, kWideStages>(kv_map, a);
+}
+static_assert((kConsumerWarps + 1) * 32 == 160 && (kWideWarps + 1) * 32 == 288,
+              "launch bounds follow the warp counts");
+
 // ------------------------------------------------------------------ host side
 
 int encode_kv_map(CUtensorMap* map, void* pool, int64_t pool_blocks, int hkv);  // runtime.cu
@@ -465,12 +496,16 @@ static cudaError_t attn_init_once() {
   if (e != cudaSuccess) return e;
   e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(paged_gqa_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)kAttnSmemBytes);
+  e = cudaFuncSetAttribute(paged_gqa_decode_kernel,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAttnSmemBytes);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(paged_gqa_decode_wide_kernel,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)attn_smem_bytes<kWideWarps, kWideStages>());
   if (e != cudaSuccess) return e;
   int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, paged_gqa_decode_kernel, kAttnThreads,
-                                                    kAttnSmemBytes);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, paged_gqa_decode_kernel,
+                                                    kAttnThreads, kAttnSmemBytes);
   if (e != cudaSuccess) return e;
   g_attn_occupancy = occ > 0 ? occ : 1;
   return cudaSuccess;
@@ -699,16 +734,21 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
   a.trace = k1_trace_buffer();
   a.trace_ctas = a.trace ? k1_trace_capacity() : 0;
   dim3 grid(plan.max_splits, hkv, batch);
+  // one wave at one CTA per SM: the wide instantiation (OFB_K1_WIDE=0|1 pins it)
+  const long ctas = (long)plan.max_splits * hkv * batch;
+  static const int wide_env = std::getenv("OFB_K1_WIDE") ? std::atoi(std::getenv("OFB_K1_WIDE")) : -1;
+  const bool wide = wide_env >= 0 ? wide_env == 1 : ctas <= g_num_sms;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
-  cfg.blockDim = dim3(kAttnThreads);
-  cfg.dynamicSmemBytes = kAttnSmemBytes;
+  cfg.blockDim = dim3(wide ? (kWideWarps + 1) * 32 : kAttnThreads);
+  cfg.dynamicSmemBytes = wide ? attn_smem_bytes<kWideWarps, kWideStages>() : kAttnSmemBytes;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  if (wide) return cudaLaunchKernelEx(&cfg, paged_gqa_decode_wide_kernel, map, a);
   return cudaLaunchKernelEx(&cfg, paged_gqa_decode_kernel, map, a);
 }
 

@@ -1,0 +1,141 @@
+// Decoder glue around the data path for the whole-decoder TP step (SURVEY.md
+// 8(d) cfg4): RMSNorm of the residual stream and the SwiGLU activation.  Not
+// among the four north-star pieces - they exist so the 70B step streams every
+// weight byte with as few launches as possible (the residual add itself is
+// folded into K6, ofb_oproj_desc.residual).
+//
+//   rmsnorm:  a[b] = x[b] / sqrt(mean(x[b]^2) + eps) * w        (one CTA per row)
+//   silu_mul: act[b, i] = silu(gu[b, i]) * gu[b, inter + i]      (grid-stride)
+#include "common.cuh"
+
+#include "../../include/orbitflow_b200.h"
+
+namespace ofb {
+int report_error(int code, const char* msg);
+int report_cuda(cudaError_t e, const char* what);
+
+namespace {
+
+constexpr int kNormThreads = 512;
+
+__device__ __forceinline__ void unpack8(uint4 u, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 v = __bfloat1622float2(h[i]);
+    f[2 * i] = v.x;
+    f[2 * i + 1] = v.y;
+  }
+}
+
+// One CTA per row; each thread holds up to kPer 8-element vectors in registers.
+template <int kPer>
+__global__ void __launch_bounds__(kNormThreads)
+rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
+               __nv_bfloat16* __restrict__ out, int hidden, float eps) {
+  const int row = blockIdx.x;
+  const int nvec = hidden / 8;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(row) * hidden);
+  float v[kPer][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int i = threadIdx.x + k * kNormThreads;
+    if (i < nvec) {
+      unpack8(xr[i], v[k]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) ss += v[k][e] * v[k][e];
+    }
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+  __shared__ float part[kNormThreads / 32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int i = 0; i < kNormThreads / 32; ++i) tot += part[i];
+  const float r = rsqrtf(tot / hidden + eps);
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  uint4* orow = reinterpret_cast<uint4*>(out + static_cast<size_t>(row) * hidden);
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int i = threadIdx.x + k * kNormThreads;
+    if (i < nvec) {
+      float g[8];
+      unpack8(wr[i], g);
+      uint4 o;
+      o.x = pack_bf16(v[k][0] * r * g[0], v[k][1] * r * g[1]);
+      o.y = pack_bf16(v[k][2] * r * g[2], v[k][3] * r * g[3]);
+      o.z = pack_bf16(v[k][4] * r * g[4], v[k][5] * r * g[5]);
+      o.w = pack_bf16(v[k][6] * r * g[6], v[k][7] * r * g[7]);
+      orow[i] = o;
+    }
+  }
+}
+
+__global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ act,
+                                int batch, int inter) {
+  const int nvec = inter / 8;
+  const size_t total = static_cast<size_t>(batch) * nvec;
+  for (size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t b = t / nvec, i = t - b * nvec;
+    const uint4* row = reinterpret_cast<const uint4*>(gu + b * 2 * inter);
+    float g[8], u[8];
+    unpack8(row[i], g);
+    unpack8(row[nvec + i], u);
+    float o[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = g[e] / (1.f + __expf(-g[e])) * u[e];
+    uint4 p;
+    p.x = pack_bf16(o[0], o[1]);
+    p.y = pack_bf16(o[2], o[3]);
+    p.z = pack_bf16(o[4], o[5]);
+    p.w = pack_bf16(o[6], o[7]);
+    reinterpret_cast<uint4*>(act + b * inter)[i] = p;
+  }
+}
+
+}  // namespace
+}  // namespace ofb
+
+extern "C" {
+
+int ofb_rmsnorm(const void* x, const void* weight, void* out, int32_t rows, int32_t hidden, float eps,
+                void* stream) {
+  using namespace ofb;
+  if (!x || !weight || !out || rows < 0) return report_error(-1, "ofb_rmsnorm: bad arguments");
+  if (hidden <= 0 || hidden % 8 || hidden > 8 * kNormThreads * 4)
+    return report_error(-1, "ofb_rmsnorm: hidden must be a multiple of 8 and <= 16384");
+  if (rows == 0) return 0;
+  auto s = static_cast<cudaStream_t>(stream);
+  const int per = (hidden / 8 + kNormThreads - 1) / kNormThreads;
+  const auto* xp = static_cast<const __nv_bfloat16*>(x);
+  const auto* wp = static_cast<const __nv_bfloat16*>(weight);
+  auto* op = static_cast<__nv_bfloat16*>(out);
+  if (per <= 1)
+    rmsnorm_kernel<1><<<rows, kNormThreads, 0, s>>>(xp, wp, op, hidden, eps);
+  else if (per <= 2)
+    rmsnorm_kernel<2><<<rows, kNormThreads, 0, s>>>(xp, wp, op, hidden, eps);
+  else
+    rmsnorm_kernel<4><<<rows, kNormThreads, 0, s>>>(xp, wp, op, hidden, eps);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : report_cuda(e, "rmsnorm_kernel launch");
+}
+
+int ofb_silu_mul(const void* gate_up, void* act, int32_t batch, int32_t inter, void* stream) {
+  using namespace ofb;
+  if (!gate_up || !act || batch < 0 || inter <= 0 || inter % 8)
+    return report_error(-1, "ofb_silu_mul: bad arguments (inter must be a multiple of 8)");
+  if (batch == 0) return 0;
+  const size_t total = static_cast<size_t>(batch) * (inter / 8);
+  int blocks = static_cast<int>((total + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  silu_mul_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(gate_up), static_cast<__nv_bfloat16*>(act), batch, inter);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : report_cuda(e, "silu_mul_kernel launch");
+}
+
+}  // extern "C"

@@ -61,7 +61,11 @@ struct OprojArgs {
   int* status;
   char* symm[kMaxPeers];
   long long flags_off;
-  unsigned long long* trace;   // diagnostics (ofb_k6_trace): per CTA stamps, or null      // byte offset of the flags inside a symmetric buffer
+  unsigned long long* trace;   // diagnostics (ofb_k6_trace): per CTA stamps, or null
+  const __nv_bfloat16* residual;   // added before the final rounding, or null (may alias out)
+  int parts;                       // > 1: column ranges written to separate tensors (world 1)
+  int part_lo[5];                  // first column of range i (part_lo[parts] = hidden)
+  __nv_bfloat16* part_out[4];
 };
 
 // ---------------------------------------------------------------- tcgen05
@@ -320,6 +324,14 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
 #pragma unroll
       for (int j = 0; j < 32; ++j) acc[j] += src[j * kTileM];
     }
+    if (a.world == 1 && a.residual) {   // x += o_proj(attn): one rounding of x + sum
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int b = c * 32 + j;
+        if (b < a.batch)
+          acc[j] += __bfloat162float(a.residual[static_cast<size_t>(b) * a.hidden + tile * kTileM + m]);
+      }
+    }
 #pragma unroll
     for (int j = 0; j < 32; ++j) stg[(c * 32 + j) * kTileM + m] = __float2bfloat16_rn(acc[j]);
   }
@@ -331,9 +343,18 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
   const uint4* s4 = reinterpret_cast<const uint4*>(stg);
   if (tr) tr[4] = globaltimer();
   if (a.world == 1) {
+    // the column range (tensor) this tile belongs to: one lookup per CTA
+    __nv_bfloat16* dst_base = a.out;
+    int dst_stride = a.hidden, col0 = tile * kTileM;
+    for (int r = 0; r < a.parts; ++r)
+      if (col0 >= a.part_lo[r] && col0 < a.part_lo[r + 1]) {
+        dst_base = a.part_out[r];
+        dst_stride = a.part_lo[r + 1] - a.part_lo[r];
+        col0 -= a.part_lo[r];
+      }
     for (int i = threadIdx.x; i < nvec; i += kThreads) {
       const int b = i >> 4, o = i & 15;
-      *reinterpret_cast<uint4*>(a.out + static_cast<size_t>(b) * a.hidden + tile * kTileM + o * 8) = s4[i];
+      *reinterpret_cast<uint4*>(dst_base + static_cast<size_t>(b) * dst_stride + col0 + o * 8) = s4[i];
     }
     if (tr) tr[5] = globaltimer();
     return;
@@ -385,6 +406,17 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
       }
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) add_bf16x8(acc[u], t[u]);
+    }
+    if (a.residual) {                  // every rank adds the same residual after the sum
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int i = i0 + u * kThreads;
+        if (i < nvec) {
+          const int b = i >> 4, q = i & 15;
+          add_bf16x8(acc[u], *reinterpret_cast<const uint4*>(
+                                 a.residual + static_cast<size_t>(b) * a.hidden + tile * kTileM + q * 8));
+        }
+      }
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
@@ -603,7 +635,7 @@ int64_t ofb_oproj_workspace_bytes(int32_t max_batch, int32_t k, int32_t hidden) 
 int ofb_oproj_allreduce(const ofb_oproj_desc* d, void* stream) {
   using namespace ofb;
   if (!d) return report_error(-1, "ofb_oproj_allreduce: null descriptor");
-  if (!d->x || !d->w || !d->out)
+  if (!d->x || !d->w || (!d->out && d->out_parts <= 1))
     return report_error(-1, "ofb_oproj_allreduce: null tensor");
   if (d->batch < 1 || d->batch > d->max_batch || d->max_batch > 256)
     return report_error(-1, "ofb_oproj_allreduce: need 1 <= batch <= max_batch <= 256");
@@ -648,6 +680,22 @@ int ofb_oproj_allreduce(const ofb_oproj_desc* d, void* stream) {
   a.status = d->status;
   for (int r = 0; r < d->world; ++r) a.symm[r] = static_cast<char*>(d->symm[r]);
   a.trace = g_k6_trace;
+  a.residual = static_cast<const __nv_bfloat16*>(d->residual);
+  a.parts = d->out_parts > 1 ? d->out_parts : 0;
+  if (a.parts) {
+    if (d->world != 1 || d->residual || a.parts > 4)
+      return report_error(-1, "ofb_oproj_allreduce: out_parts needs world 1, no residual, <= 4 parts");
+    int lo = 0;
+    for (int r = 0; r < a.parts; ++r) {
+      if (!d->part_out[r] || d->part_cols[r] <= 0 || d->part_cols[r] % kTileM)
+        return report_error(-1, "ofb_oproj_allreduce: part_cols must be positive multiples of 128");
+      a.part_lo[r] = lo;
+      a.part_out[r] = static_cast<__nv_bfloat16*>(d->part_out[r]);
+      lo += d->part_cols[r];
+    }
+    a.part_lo[a.parts] = lo;
+    if (lo != d->hidden) return report_error(-1, "ofb_oproj_allreduce: part_cols must sum to hidden");
+  }
   a.flags_off = static_cast<long long>((inbox_bytes(d->world, d->max_batch, d->hidden) + 255) / 256 * 256);
 
   const size_t smem = static_cast<size_t>(a.stages) * stage_bytes + red_bytes(splits, npad) + 1024;

@@ -241,9 +241,15 @@ class TensorParallelLlama:
             return out
 
         qkv_rows = (hq + 2 * hkv) * 128
-        self.w_qkv = rand((L, qkv_rows, hidden), hidden)            # Linear layout [out, in]
-        self.w_gu = rand((L, 2 * self.inter, hidden), hidden)
         packed = c1 == "k6"
+        # with K6 every projection runs on it (the column-parallel q/k/v and
+        # gate/up ones with world 1: no exchange); the NCCL arm is the cuBLAS
+        # baseline throughout
+        self.w_qkv = rand((L, qkv_rows, hidden), hidden, packed)
+        self.w_gu = rand((L, 2 * self.inter, hidden), hidden, packed)
+        if packed:
+            self.qkv_proj = OprojAllReduce(self.w_qkv, max_batch)
+            self.gu_proj = OprojAllReduce(self.w_gu, max_batch)
         w_o = rand((L, hidden, hq * 128), shard.num_q_heads * 128, packed)
         w_d = rand((L, hidden, self.inter), intermediate, packed)
         self.norm = torch.ones((2, hidden), dtype=torch.bfloat16, device=dev)
@@ -264,19 +270,18 @@ class TensorParallelLlama:
     def layer_weights(self, l: int) -> dict:
         """Layer ``l``'s weights in ``nn.Linear`` layout [out, in] (test / reference use)."""
         nq, nk = self.shard.local_q * 128, self.shard.local_kv * 128
-        w = self.w_qkv[l]
 
-        def unpack(proj):
-            t = proj.w[l]
-            if proj.w_layout == 0:
+        def unpack(t):
+            if t.dim() == 2:
                 return t
             tiles, chunks = t.shape[:2]
             return t.permute(0, 2, 1, 3).reshape(tiles * 128, chunks * 64)
 
-        o = unpack(self.oproj) if self.c1 == "k6" else self.w_o[l]
-        d = unpack(self.down) if self.c1 == "k6" else self.w_d[l]
+        w, gu = unpack(self.w_qkv[l]), unpack(self.w_gu[l])
+        o = unpack(self.oproj.w[l]) if self.c1 == "k6" else self.w_o[l]
+        d = unpack(self.down.w[l]) if self.c1 == "k6" else self.w_d[l]
         return {"q": w[:nq], "k": w[nq:nq + nk], "v": w[nq + nk:], "o": o,
-                "gate": self.w_gu[l, : self.inter], "up": self.w_gu[l, self.inter:], "down": d}
+                "gate": gu[: self.inter], "up": gu[self.inter:], "down": d}
 
     @property
     def weight_bytes(self) -> int:
@@ -293,24 +298,41 @@ class TensorParallelLlama:
             mk = lambda *s: torch.empty(s, dtype=torch.bfloat16, device=dev)  # noqa: E731
             self._bufs = {"B": B, "q": mk(L, B, hq, 128), "k_new": mk(L, B, hkv, 128),
                           "v_new": mk(L, B, hkv, 128), "act": mk(L, B, self.inter),
-                          "h": mk(B, self.hidden), "x": [mk(B, self.hidden), mk(B, self.hidden)]}
+                          "h": mk(B, self.hidden), "x": [mk(B, self.hidden), mk(B, self.hidden)],
+                          "a": mk(L, B, self.hidden), "a2": mk(L, B, self.hidden),
+                          "gu": mk(B, 2 * self.inter)}
         return self._bufs
 
-    def _reduce(self, proj, w, x_all, l, out, stream):
-        """out = sum over ranks of x_all[l] @ w[l]^T (C1)."""
+    def _reduce(self, proj, w, x_all, l, x, h, stream):
+        """x += sum over ranks of x_all[l] @ w[l]^T (C1).  K6 folds the residual
+        add into its epilogue; the NCCL arm projects into ``h``, all-reduces it
+        and adds."""
         if self.c1 == "k6":
-            proj(x_all, l, out=out, stream=stream)
+            proj(x_all, l, out=x, stream=stream, residual=x)
             return
-        torch.matmul(x_all[l].reshape(out.shape[0], -1), w[l].t(), out=out)
+        torch.matmul(x_all[l].reshape(h.shape[0], -1), w[l].t(), out=h)
         if self.world > 1:
             import torch.distributed as dist
 
-            dist.all_reduce(out, group=self.group)
+            dist.all_reduce(h, group=self.group)
+        x.add_(h)
+
+    def _rmsnorm(self, x, weight, out, stream):
+        from . import _native
+
+        _native.check(_native.load().ofb_rmsnorm(x.data_ptr(), weight.data_ptr(), out.data_ptr(),
+                                                 x.shape[0], self.hidden, float(self.eps),
+                                                 stream.cuda_stream), "ofb_rmsnorm")
+
+    def _silu_mul(self, gu, act, stream):
+        from . import _native
+
+        _native.check(_native.load().ofb_silu_mul(gu.data_ptr(), act.data_ptr(), gu.shape[0],
+                                                  self.inter, stream.cuda_stream), "ofb_silu_mul")
 
     def step(self, batch, x_in: torch.Tensor) -> torch.Tensor:
         """One decode step of the whole decoder; ``x_in`` bf16 [B, hidden] (the
         new tokens' embeddings).  Returns the final hidden state [B, hidden]."""
-        import torch.nn.functional as F
 
         ex = self.ex
         B, L = len(batch), ex.shape.num_layers
@@ -326,24 +348,33 @@ class TensorParallelLlama:
         x.copy_(x_in)
         h = bufs["h"]
         nq, nk = self.shard.local_q * 128, self.shard.local_kv * 128
+        a_all, a2_all, gu = bufs["a"], bufs["a2"], bufs["gu"]
+        k6 = self.c1 == "k6"
         ex.runtime.step_begin(desc, stream)
         try:
             for l in range(L):
-                a = F.rms_norm(x, (self.hidden,), self.norm[0], self.eps)
-                w = self.w_qkv[l]
-                torch.matmul(a, w[:nq].t(), out=q[l].view(B, nq))
-                torch.matmul(a, w[nq:nq + nk].t(), out=kn[l].view(B, nk))
-                torch.matmul(a, w[nq + nk:].t(), out=vn[l].view(B, nk))
+                a = a_all[l]
+                self._rmsnorm(x, self.norm[0], a, stream)
+                if k6:     # q / k / v of this rank's heads in one launch, into their buffers
+                    self.qkv_proj(a_all, l, stream=stream,
+                                  parts=[q[l].view(B, nq), kn[l].view(B, nk), vn[l].view(B, nk)])
+                else:
+                    w = self.w_qkv[l]
+                    torch.matmul(a, w[:nq].t(), out=q[l].view(B, nq))
+                    torch.matmul(a, w[nq:nq + nk].t(), out=kn[l].view(B, nk))
+                    torch.matmul(a, w[nq + nk:].t(), out=vn[l].view(B, nk))
                 ex.runtime.step_layers(1)                    # K3 + K2 wait + K1 of layer l
-                self._reduce(getattr(self, "oproj", None), getattr(self, "w_o", None), out, l, h,
-                             stream)
-                x.add_(h)
-                a = F.rms_norm(x, (self.hidden,), self.norm[1], self.eps)
-                gu = torch.matmul(a, self.w_gu[l].t())
-                torch.mul(F.silu(gu[:, : self.inter]), gu[:, self.inter:], out=bufs["act"][l])
+                self._reduce(getattr(self, "oproj", None), getattr(self, "w_o", None), out, l, x, h,
+                             stream)                         # x += o_proj(attn) (C1)
+                a2 = a2_all[l]
+                self._rmsnorm(x, self.norm[1], a2, stream)
+                if k6:
+                    self.gu_proj(a2_all, l, out=gu, stream=stream)
+                else:
+                    torch.matmul(a2, self.w_gu[l].t(), out=gu)
+                self._silu_mul(gu, bufs["act"][l], stream)
                 self._reduce(getattr(self, "down", None), getattr(self, "w_d", None), bufs["act"],
-                             l, h, stream)
-                x.add_(h)
+                             l, x, h, stream)                # x += down(act) (C1)
         except BaseException:
             ex.runtime.step_abort()
             raise

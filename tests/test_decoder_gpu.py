@@ -259,3 +259,27 @@ def test_step_abort_keeps_runtime_usable():
     finally:
         tpd.close()
         ex.close()
+
+
+@pytest.mark.parametrize("rows,hidden", [(32, 8192), (3, 4096), (1, 1024), (5, 16384)])
+def test_rmsnorm_and_silu_mul_glue_match_fp32(rows, hidden):
+    """The decoder glue kernels (ofb_rmsnorm, ofb_silu_mul) vs fp32 torch."""
+    from paper_2601_10729_b200 import _native
+
+    lib = _native.load()
+    dev = torch.device("cuda:0")
+    g = torch.Generator(device=dev).manual_seed(rows + hidden)
+    x = torch.randn((rows, hidden), generator=g, device=dev).to(torch.bfloat16)
+    w = (1 + 0.1 * torch.randn((hidden,), generator=g, device=dev)).to(torch.bfloat16)
+    out = torch.empty_like(x)
+    s = torch.cuda.current_stream().cuda_stream
+    _native.check(lib.ofb_rmsnorm(x.data_ptr(), w.data_ptr(), out.data_ptr(), rows, hidden, 1e-5, s),
+                  "ofb_rmsnorm")
+    want = _rms(x.float()) * w.float()
+    torch.testing.assert_close(out.float(), want, rtol=2e-2, atol=1e-2)
+    inter = hidden // 2
+    gu = torch.randn((rows, 2 * inter), generator=g, device=dev).to(torch.bfloat16)
+    act = torch.empty((rows, inter), dtype=torch.bfloat16, device=dev)
+    _native.check(lib.ofb_silu_mul(gu.data_ptr(), act.data_ptr(), rows, inter, s), "ofb_silu_mul")
+    want = F.silu(gu[:, :inter].float()) * gu[:, inter:].float()
+    torch.testing.assert_close(act.float(), want, rtol=2e-2, atol=1e-2)

@@ -187,3 +187,41 @@ def test_two_processes_exchange_ipc_handles_on_one_gpu():
     for call, raw in enumerate(res[0]):
         got = torch.from_numpy(np.frombuffer(raw, dtype=np.int16).copy()).view(torch.bfloat16).view(b, h)
         torch.testing.assert_close(got.float(), _want(xs, ws, call % 2), rtol=RTOL, atol=ATOL)
+
+
+def test_column_parts_equal_the_single_output():
+    """One K6 launch writing the q / k / v column ranges straight into three
+    tensors gives exactly the columns of the single-output projection."""
+    from paper_2601_10729_b200.collective import OprojAllReduce
+
+    dev = torch.device("cuda:0")
+    b, k, h = 5, 512, 128 * 10           # 8 q tiles + 1 k tile + 1 v tile
+    xs, ws = _inputs(1, 2, b, k, h, seed=21)
+    op = OprojAllReduce(ws[0].to(dev), b)
+    x = xs[0].to(dev)
+    whole = op(x, 1)
+    qv = torch.empty((b, 1024), dtype=torch.bfloat16, device=dev)
+    kv = torch.empty((b, 128), dtype=torch.bfloat16, device=dev)
+    vv = torch.empty((b, 128), dtype=torch.bfloat16, device=dev)
+    op(x, 1, parts=[qv, kv, vv])
+    torch.cuda.synchronize()
+    assert torch.equal(qv, whole[:, :1024])
+    assert torch.equal(kv, whole[:, 1024:1152])
+    assert torch.equal(vv, whole[:, 1152:])
+    with pytest.raises(ValueError):
+        op(x, 1, parts=[qv, kv])          # columns do not add up to hidden
+
+
+def test_fused_residual_adds_before_the_rounding():
+    from paper_2601_10729_b200.collective import OprojAllReduce
+
+    dev = torch.device("cuda:0")
+    b, k, h = 7, 256, 512
+    xs, ws = _inputs(1, 1, b, k, h, seed=31)
+    op = OprojAllReduce(ws[0].to(dev), b)
+    resid = torch.randn((b, h), device=dev).to(torch.bfloat16)
+    want = resid.float() + xs[0][0].to(dev).float() @ ws[0][0].to(dev).float().T
+    x_res = resid.clone()
+    op(xs[0].to(dev), 0, out=x_res, residual=x_res)       # in place: x += proj
+    torch.cuda.synchronize()
+    torch.testing.assert_close(x_res.float(), want, rtol=RTOL, atol=ATOL)

@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--layers", type=int, default=80)
     ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--c1", default="k6")
+    ap.add_argument("--profile-last", action="store_true",
+                    help="cudaProfilerStart/Stop around the last step (ncu --profile-from-start off)")
     args = ap.parse_args()
     shard = HeadShard(0, args.tp, 64, 8)
     shape = ModelShape(args.layers, shard.local_q, shard.local_kv)
@@ -44,7 +46,13 @@ def main():
     torch.cuda.synchronize()
     evs[0].record()
     for i in range(args.steps):
+        if args.profile_last and i == args.steps - 1:
+            torch.cuda.synchronize()
+            torch.cuda.profiler.start()
         dec.step(batch, x)
+        if args.profile_last and i == args.steps - 1:
+            torch.cuda.synchronize()
+            torch.cuda.profiler.stop()
         evs[i + 1].record()
         for r in batch:
             r.record_generated_token()
