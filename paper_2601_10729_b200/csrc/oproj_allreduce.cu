@@ -212,6 +212,7 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
   const int stage_w = kTileM * kChunkK * 2;          // 16 KiB of W rows
   const int stage_bytes = stage_w + a.npad * kChunkK * 2;
   const uint32_t tcols = a.npad <= 32 ? 32u : a.npad <= 64 ? 64u : a.npad <= 128 ? 128u : 256u;
+  const int pre = nchunks < a.stages ? nchunks : a.stages;
 
   if (threadIdx.x == 0) {
     prefetch_tma_desc(&wmap);
@@ -222,6 +223,14 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
     }
     mbar_init(&acc_bar, 1);
     fence_mbar_init();
+    // W_o does not depend on the previous kernel (attention), so the first
+    // ring's worth of weight tiles is requested first thing - before the TMEM
+    // allocation and the CTA barrier, and before the programmatic-dependent-
+    // launch wait; x (the attention output) after it.
+    for (int i = 0; i < pre; ++i) {
+      mbar_arrive_expect_tx(&full_bar[i], stage_bytes);
+      tma_load_4d(smem + i * stage_bytes, &wmap, &full_bar[i], 0, 0, c0 + i, a.layer * a.tiles + tile);
+    }
   }
   __syncwarp();   // warp 0 re-converges after its lane-0 setup before the aligned barrier
   if (warp == 2) tmem_alloc(&tmem_base_sh, tcols);
@@ -236,14 +245,7 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
   if (tr) tr[1] = globaltimer();
 
   if (warp == 0 && lane == 0) {
-    // TMA producer.  W_o does not depend on the previous kernel (attention), so
-    // the first ring's worth of weight tiles is requested before the
-    // programmatic-dependent-launch wait; x (the attention output) after it.
-    const int pre = nchunks < a.stages ? nchunks : a.stages;
-    for (int i = 0; i < pre; ++i) {
-      mbar_arrive_expect_tx(&full_bar[i], stage_bytes);
-      tma_load_4d(smem + i * stage_bytes, &wmap, &full_bar[i], 0, 0, c0 + i, a.layer * a.tiles + tile);
-    }
+    // TMA producer: the first stages' W loads are in flight (above)
     pdl_wait();
     for (int i = 0; i < pre; ++i)
       tma_load_3d(smem + i * stage_bytes + stage_w, &xmap, &full_bar[i], (c0 + i) * kChunkK, 0, a.layer);

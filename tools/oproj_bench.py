@@ -27,6 +27,10 @@ SHAPES = [  # name, B, K, H
     ("70B TP1", 32, 8192, 8192),
     ("8B TP1 B16", 16, 4096, 4096),
     ("8B TP4 B16", 16, 1024, 4096),
+    # the other projections of the 70B TP8 decoder step (same kernel, world 1)
+    ("70B TP8 qkv", 32, 8192, 1280),
+    ("70B TP8 gate_up", 32, 8192, 7168),
+    ("70B TP8 down", 32, 3584, 8192),
 ]
 
 
