@@ -128,36 +128,45 @@ __device__ __forceinline__ void attend_tile(WarpAttnState& st, const uint32_t (&
   }
 }
 
-// Warp-state exchange buffer for merging the consumer warps of one CTA.
+// Warp-state exchange buffer for merging the consumer warps of one CTA.  Row
+// stride 136 floats: a warp's float2 stores of 4 rows x 8 dims fill the 32
+// banks exactly (two wavefronts per 8 rows, no conflicts).
+constexpr int kMergeStride = kHeadDim + 8;
 template <int kWarps>
 struct MergeSlots {
-  float o[kWarps][kMaxGroup][kHeadDim + 4];
+  float o[kWarps][kMaxGroup][kMergeStride];
   float m[kWarps][kMaxGroup];
   float l[kWarps][kMaxGroup];
 };
 
+// Only the g real query rows are published (the mma pads the group to 16 rows):
+// at g = 4 that is a quarter of the stores.
 template <int kWarps>
 __device__ __forceinline__ void publish_state(MergeSlots<kWarps>* ms, WarpAttnState& st, int warp,
-                                              int lane) {
+                                              int lane, int g) {
   float l0 = st.l[0], l1 = st.l[1];
   l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
   l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
   const int r0 = lane >> 2, c0 = (lane & 3) * 2;
+  if (r0 < g) {
 #pragma unroll
-  for (int nt = 0; nt < 16; ++nt) {
-    const int d = nt * 8 + c0;
-    ms->o[warp][r0][d] = st.o[nt][0];
-    ms->o[warp][r0][d + 1] = st.o[nt][1];
-    ms->o[warp][r0 + 8][d] = st.o[nt][2];
-    ms->o[warp][r0 + 8][d + 1] = st.o[nt][3];
+    for (int nt = 0; nt < 16; ++nt)
+      *reinterpret_cast<float2*>(&ms->o[warp][r0][nt * 8 + c0]) = make_float2(st.o[nt][0], st.o[nt][1]);
+    if ((lane & 3) == 0) {
+      ms->m[warp][r0] = st.m[0];
+      ms->l[warp][r0] = l0;
+    }
   }
-  if ((lane & 3) == 0) {
-    ms->m[warp][r0] = st.m[0];
-    ms->l[warp][r0] = l0;
-    ms->m[warp][r0 + 8] = st.m[1];
-    ms->l[warp][r0 + 8] = l1;
+  if (r0 + 8 < g) {
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt)
+      *reinterpret_cast<float2*>(&ms->o[warp][r0 + 8][nt * 8 + c0]) = make_float2(st.o[nt][2], st.o[nt][3]);
+    if ((lane & 3) == 0) {
+      ms->m[warp][r0 + 8] = st.m[1];
+      ms->l[warp][r0 + 8] = l1;
+    }
   }
 }
 

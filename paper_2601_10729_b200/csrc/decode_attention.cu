@@ -330,18 +330,24 @@ __device__ __forceinline__ void paged_gqa_decode_body(const CUtensorMap& kv_map,
   MergeSlots<kW>* ms = reinterpret_cast<MergeSlots<kW>*>(ring);
   MergeWeights<kW>* mwt = reinterpret_cast<MergeWeights<kW>*>(
       ring + sizeof(MergeSlots<kW>));
-  if (warp < kW) {
+  if (warp < kW) {   // only the g real query rows (the mma pads the group to 16)
+    if (r0 < g) {
 #pragma unroll
-    for (int nt = 0; nt < 16; ++nt) {
-      const int d = nt * 8 + c0;
-      *reinterpret_cast<float2*>(&ms->o[warp][r0][d]) = make_float2(o[nt][0], o[nt][1]);
-      *reinterpret_cast<float2*>(&ms->o[warp][r0 + 8][d]) = make_float2(o[nt][2], o[nt][3]);
+      for (int nt = 0; nt < 16; ++nt)
+        *reinterpret_cast<float2*>(&ms->o[warp][r0][nt * 8 + c0]) = make_float2(o[nt][0], o[nt][1]);
+      if ((lane & 3) == 0) {
+        ms->m[warp][r0] = m_run[0];
+        ms->l[warp][r0] = l_run[0];
+      }
     }
-    if ((lane & 3) == 0) {
-      ms->m[warp][r0] = m_run[0];
-      ms->l[warp][r0] = l_run[0];
-      ms->m[warp][r0 + 8] = m_run[1];
-      ms->l[warp][r0 + 8] = l_run[1];
+    if (r0 + 8 < g) {
+#pragma unroll
+      for (int nt = 0; nt < 16; ++nt)
+        *reinterpret_cast<float2*>(&ms->o[warp][r0 + 8][nt * 8 + c0]) = make_float2(o[nt][2], o[nt][3]);
+      if ((lane & 3) == 0) {
+        ms->m[warp][r0 + 8] = m_run[1];
+        ms->l[warp][r0 + 8] = l_run[1];
+      }
     }
   }
   __syncthreads();

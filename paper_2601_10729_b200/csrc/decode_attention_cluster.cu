@@ -189,7 +189,7 @@ paged_gqa_decode_cluster_kernel(const __grid_constant__ CUtensorMap kv_map, cons
   MergeSlots<kCWarps>* ms = reinterpret_cast<MergeSlots<kCWarps>*>(ring);
   MergeWeights<kCWarps>* mwt =
       reinterpret_cast<MergeWeights<kCWarps>*>(ring + sizeof(MergeSlots<kCWarps>));
-  if (warp < kCWarps) publish_state<kCWarps>(ms, st, warp, lane);
+  if (warp < kCWarps) publish_state<kCWarps>(ms, st, warp, lane, g);
   __syncthreads();
   merge_weights<kCWarps>(ms, mwt, g, tid);
   __syncthreads();

@@ -244,7 +244,7 @@ paged_gqa_decode_stream_kernel(const __grid_constant__ CUtensorMap kv_map, const
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    publish_state(ms, st, warp, lane);
+    publish_state(ms, st, warp, lane, g);
     consumer_bar();
 
     const bool whole = (pb >= begin) && (pe <= end);

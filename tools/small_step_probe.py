@@ -1,5 +1,7 @@
 """All-resident decode steps at small batch (the cfg3 regime): device time per
-step for the 8B shape, B in {1, 4}, 16K context, stream-launched and pipelined.
+step for the 8B shape and the 70B TP8 rank shard (8 q / 1 KV head), B in {1, 4},
+4K and 16K context, stream-launched and pipelined: the per-layer K1 cost inside
+a step (K1 of a layer without a fetch streams its KV before the PDL wait).
 Run once as is and once with OFB_PDL=0 to see what programmatic dependent launch
 (+ kv_ready KV streaming before the wait) buys when each layer is short."""
 import json
@@ -13,9 +15,10 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2601_10729_b200.core import PlacementMatrix, RequestState  # noqa: E402
 from paper_2601_10729_b200.executor import B200Executor, ModelShape  # noqa: E402
 
-shape = ModelShape(32, 32, 8)
-for B in (1, 4):
-    ctx = 16384
+import itertools  # noqa: E402
+
+for (name, shape), B, ctx in itertools.product(
+        [("8B", ModelShape(32, 32, 8)), ("70B-TP8-shard", ModelShape(32, 8, 1))], (1, 4), (4096, 16384)):
     cap = -(-(ctx + 64 + 1) // 16)
     batch = [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=ctx, target_output_tokens=64)
              for i in range(B)]
@@ -34,6 +37,6 @@ for B in (1, 4):
     ex.drain()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 40
-    print(json.dumps({"B": B, "context": ctx, "pdl": os.environ.get("OFB_PDL", "1"),
+    print(json.dumps({"shape": name, "B": B, "context": ctx, "pdl": os.environ.get("OFB_PDL", "1"),
                       "ms_per_step": ms, "us_per_layer": ms * 1e3 / 32}), flush=True)
     ex.close()
