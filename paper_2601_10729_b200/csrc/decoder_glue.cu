@@ -33,6 +33,8 @@ template <int kPer>
 __global__ void __launch_bounds__(kNormThreads)
 rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
                __nv_bfloat16* __restrict__ out, int hidden, float eps) {
+  pdl_wait();      // x is the previous kernel's output
+  pdl_trigger();   // the next projection may start streaming its weights
   const int row = blockIdx.x;
   const int nvec = hidden / 8;
   const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(row) * hidden);
@@ -76,6 +78,8 @@ rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restr
 
 __global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ act,
                                 int batch, int inter) {
+  pdl_wait();
+  pdl_trigger();
   const int nvec = inter / 8;
   const size_t total = static_cast<size_t>(batch) * nvec;
   for (size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; t < total;
@@ -97,6 +101,23 @@ __global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloa
   }
 }
 
+// Launch with programmatic stream serialization (unless OFB_PDL=0): the glue
+// kernels wait for their predecessor before reading anything and release their
+// dependent at once, so the next K6 requests its weight ring while they run.
+template <typename... Params, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(Params...), int grid, int block, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 }  // namespace
 }  // namespace ofb
 
@@ -114,13 +135,9 @@ int ofb_rmsnorm(const void* x, const void* weight, void* out, int32_t rows, int3
   const auto* xp = static_cast<const __nv_bfloat16*>(x);
   const auto* wp = static_cast<const __nv_bfloat16*>(weight);
   auto* op = static_cast<__nv_bfloat16*>(out);
-  if (per <= 1)
-    rmsnorm_kernel<1><<<rows, kNormThreads, 0, s>>>(xp, wp, op, hidden, eps);
-  else if (per <= 2)
-    rmsnorm_kernel<2><<<rows, kNormThreads, 0, s>>>(xp, wp, op, hidden, eps);
-  else
-    rmsnorm_kernel<4><<<rows, kNormThreads, 0, s>>>(xp, wp, op, hidden, eps);
-  const cudaError_t e = cudaGetLastError();
+  const cudaError_t e = per <= 1   ? launch_pdl(rmsnorm_kernel<1>, rows, kNormThreads, s, xp, wp, op, hidden, eps)
+                       : per <= 2 ? launch_pdl(rmsnorm_kernel<2>, rows, kNormThreads, s, xp, wp, op, hidden, eps)
+                                  : launch_pdl(rmsnorm_kernel<4>, rows, kNormThreads, s, xp, wp, op, hidden, eps);
   return e == cudaSuccess ? 0 : report_cuda(e, "rmsnorm_kernel launch");
 }
 
@@ -132,9 +149,9 @@ int ofb_silu_mul(const void* gate_up, void* act, int32_t batch, int32_t inter, v
   const size_t total = static_cast<size_t>(batch) * (inter / 8);
   int blocks = static_cast<int>((total + 255) / 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
-  silu_mul_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const __nv_bfloat16*>(gate_up), static_cast<__nv_bfloat16*>(act), batch, inter);
-  const cudaError_t e = cudaGetLastError();
+  const cudaError_t e = launch_pdl(silu_mul_kernel, blocks, 256, static_cast<cudaStream_t>(stream),
+                                   static_cast<const __nv_bfloat16*>(gate_up),
+                                   static_cast<__nv_bfloat16*>(act), batch, inter);
   return e == cudaSuccess ? 0 : report_cuda(e, "silu_mul_kernel launch");
 }
 

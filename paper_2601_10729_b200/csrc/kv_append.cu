@@ -39,6 +39,10 @@ struct AppendArgs {
 };
 
 __global__ void __launch_bounds__(256) kv_append_kernel(const AppendArgs a) {
+  // k_new / v_new may be the previous kernel's output, and it may read the pool.
+  // No early launch_dependents: the next K1 (cluster variant) would place its
+  // clusters around these CTAs and lose its one-wave fit (measured +0.5 us/layer).
+  pdl_wait();
   const int layer = blockIdx.y;
   const int pair = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (pair >= a.batch * a.hkv) return;
@@ -71,7 +75,7 @@ cudaError_t launch_kv_append(const void* k_new, const void* v_new, void* pool,
                              const int32_t* block_tables, int max_blocks,
                              const int32_t* positions, const uint64_t* host_slabs,
                              int num_layers, int batch, int hkv, int mode,
-                             cudaStream_t stream) {
+                             cudaStream_t stream, bool pdl) {
   if (batch <= 0 || num_layers <= 0) return cudaSuccess;
   AppendArgs a;
   a.k_new = static_cast<const uint4*>(k_new);
@@ -86,8 +90,21 @@ cudaError_t launch_kv_append(const void* k_new, const void* v_new, void* pool,
   a.mode = mode;
   const int warps_per_cta = 8;
   dim3 grid((batch * hkv + warps_per_cta - 1) / warps_per_cta, num_layers);
-  kv_append_kernel<<<grid, warps_per_cta * 32, 0, stream>>>(a);
-  return cudaGetLastError();
+  // `pdl`: programmatic launch (unless OFB_PDL=0) - the launch latency overlaps
+  // the predecessor's tail and the kernel itself waits for it before touching
+  // memory.  Used between the whole-decoder step's kernels (q/k/v projection ->
+  // append -> K1); the step-start append follows a timing event and stays a
+  // plain launch (programmatic there measured 16 us slower per step).
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(warps_per_cta * 32);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl && pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kv_append_kernel, a);
 }
 
 }  // namespace ofb

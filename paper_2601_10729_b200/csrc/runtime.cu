@@ -32,7 +32,7 @@ cudaError_t launch_kv_append(const void* k_new, const void* v_new, void* pool,
                              const int32_t* block_tables, int max_blocks,
                              const int32_t* positions, const uint64_t* host_slabs,
                              int num_layers, int batch, int hkv, int mode,
-                             cudaStream_t stream);
+                             cudaStream_t stream, bool pdl = false);
 int attention_occupancy();
 int set_attention_variant(int variant);
 int attention_variant_for(int batch, int hq, int hkv, int max_seq_len);
@@ -721,7 +721,8 @@ int step_layers(ofb_runtime* rt, int count) {
                                 static_cast<const uint8_t*>(d->v_new) + l * kv_layer, d->kv_pool,
                                 d->block_tables + l * bt_layer, d->max_blocks, d->positions,
                                 d->host_slabs_dev + (size_t)l * B, 1, B, d->num_kv_heads,
-                                d->append_per_layer ? /*kAppendAll*/ 1 : /*kAppendOffloaded*/ 2, cs);
+                                d->append_per_layer ? /*kAppendAll*/ 1 : /*kAppendOffloaded*/ 2, cs,
+                                /*pdl*/ d->append_per_layer && !layer_fetches);
       if (e != cudaSuccess) return cuda_fail(e, "kv_append_kernel launch");
     }
     cudaEvent_t t0 = nullptr, t1 = nullptr;
