@@ -458,14 +458,17 @@ int ring_stages(int npad, int splits) {
   return std::max(2, std::min<int>(kMaxStages, static_cast<int>(avail / stage_bytes)));
 }
 
-// CTAs per hidden tile (= cluster size): enough to cover the SMs, at most 4,
-// at most one K chunk each, and the leader's reduction buffers must fit beside
-// a ring of at least 2 stages.  (8-CTA clusters compute correctly but tripped
-// compute-sanitizer synccheck at the first barrier; 4 is where our shapes sit.)
+// CTAs per hidden tile (= cluster size): enough to cover the SMs, at most 8
+// (portable clusters), at most one K chunk each, and the leader's reduction
+// buffers must fit beside a ring of at least 2 stages.  8 splits are what the
+// narrow q/k/v projection needs (10 tiles at 70B TP8: 80 CTAs, 9.8 us vs 11.6 us
+// at 4 splits; synccheck / racecheck / memcheck clean, profiles/sanitizer/).
 int choose_splits(int tiles, int chunks, int npad) {
   int s = num_sms() / tiles;
   if (const char* f = std::getenv("OFB_K6_SPLITS")) s = std::atoi(f);   // tuning experiments
-  s = std::max(1, std::min(s, std::min(4, chunks)));
+  int cap = 8;   // portable cluster size; the leader gathers splits-1 fp32 partials
+  if (const char* f = std::getenv("OFB_K6_SPLIT_CAP")) cap = std::atoi(f);   // tuning experiments
+  s = std::max(1, std::min(s, std::min(std::min(cap, 8), chunks)));
   // the reduction buffers + a 2-stage ring must fit; the bf16 staging reuses the ring
   const int stage_bytes = kTileM * kChunkK * 2 + npad * kChunkK * 2;
   while (s > 1 && red_bytes(s, npad) + 2 * static_cast<size_t>(stage_bytes) > static_cast<size_t>(kSmemBudget))
