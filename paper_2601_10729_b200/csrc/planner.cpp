@@ -483,8 +483,14 @@ struct Ranker {
         }
       }
     };
+    // Threads only pay off on large spaces: spawning them costs ~30 us each, which
+    // made a B <= 3 solve (<= 36k candidates, microseconds of work) take 0.5 ms -
+    // the serving loop's largest host cost when it re-plans every step.
+    double space = 1.0;
+    for (int r = 0; r < B; ++r) space *= C;
+    const int workers = space < 65536.0 ? 1 : std::min<int64_t>(threads, roots);
     std::vector<std::thread> ts;
-    for (int t = 1; t < threads; ++t) ts.emplace_back(worker);
+    for (int t = 1; t < workers; ++t) ts.emplace_back(worker);
     worker();
     for (auto& th : ts) th.join();
     size_t n = 0;
