@@ -37,6 +37,7 @@ def _want(xs, ws, layer):
 @pytest.mark.parametrize("b,k,h", [
     (32, 1024, 8192),     # 70B TP8 shard: 8 q heads x 128 -> hidden 8192
     (32, 8192, 8192),     # 70B TP1
+    (32, 8192, 1280),     # 70B TP8 q/k/v projection: 10 tiles x 8-CTA clusters
     (16, 1024, 4096),     # 8B TP4
     (5, 128, 1024),       # toy, ragged batch
     (256, 256, 1024),     # max batch
@@ -134,6 +135,34 @@ def test_exchange_refuses_a_grid_the_gpu_cannot_hold_at_once():
         torch.testing.assert_close(out.float().cpu(), want, rtol=RTOL, atol=ATOL)
     finally:
         bufs[0].close()
+
+
+@pytest.mark.parametrize("splits", [1, 2, 3, 5, 8])
+def test_cluster_split_counts_agree_with_fp32(monkeypatch, splits):
+    """Every cluster size of the split-K reduction (3 and 5: non-power-of-two
+    clusters, uneven K ranges) gives the fp32 result through the plain, the
+    residual and the column-parts epilogues, and is deterministic."""
+    from paper_2601_10729_b200.collective import OprojAllReduce
+
+    dev = torch.device("cuda:0")
+    b, k, h = 19, 1280, 1280
+    xs, ws = _inputs(1, 2, b, k, h, seed=40 + splits)
+    monkeypatch.setenv("OFB_K6_SPLITS", str(splits))
+    op = OprojAllReduce(ws[0].to(dev), max_batch=32)
+    x = xs[0].to(dev)
+    want = xs[0][1].float() @ ws[0][1].float().T
+    plain = op(x, 1)
+    res = torch.randn((b, h), generator=torch.Generator().manual_seed(3)).to(torch.bfloat16)
+    out = res.to(dev).clone()
+    op(x, 1, out=out, residual=out)
+    parts = [torch.empty((b, c), dtype=torch.bfloat16, device=dev) for c in (1024, 128, 128)]
+    op(x, 1, parts=parts)
+    again = op(x, 1)
+    torch.cuda.synchronize()
+    torch.testing.assert_close(plain.float().cpu(), want, rtol=RTOL, atol=ATOL)
+    torch.testing.assert_close(out.float().cpu(), want + res.float(), rtol=RTOL, atol=ATOL)
+    assert torch.equal(torch.cat(parts, 1), plain), "parts must equal the single output bit for bit"
+    assert torch.equal(again, plain), "split-K reduction must be deterministic"
 
 
 def _ipc_worker(rank, world, port, b, k, h, q):
