@@ -306,6 +306,23 @@ typedef struct ofb_oproj_desc {
                           the q / k / v projections straight into their own buffers */
   int32_t part_cols[4];
   void* part_out[4];
+  /* Fused RMSNorm across two launches (the whole-decoder step; NULL = off):
+   * ss_out: fp32 [hidden/128][max_batch] - per hidden tile, the sum over its 128
+   *   columns of the final output^2 (after the residual add) of every batch row;
+   * ss_in (world 1): fp32 [ss_tiles][max_batch] from a previous launch's ss_out (or
+   *   ofb_row_sumsq): every output row b is scaled by rsqrt(sum_t ss_in[t][b] /
+   *   (128 ss_tiles) + eps) - RMSNorm(x) . W^T with the norm weight folded into w. */
+  float* ss_out;
+  const float* ss_in;
+  int32_t ss_tiles;
+  float eps;
+  /* swiglu = 1 (world 1, no residual / parts): w rows interleaved per 64 (gate rows
+   * 64t..64t+63, then up rows 64t..64t+63, per 128-row tile); out is bf16
+   * [batch][hidden/2] = silu(gate) * up of the rounded projections. */
+  int32_t swiglu;
+  /* x_layers: 0 = x holds `layers` layers and layer `layer` is read; 1 = x is one
+   * bf16 [batch][k] input for every layer (the decoder's residual stream). */
+  int32_t x_layers;
 } ofb_oproj_desc;
 
 OFB_API int ofb_oproj_allreduce(const ofb_oproj_desc* desc, void* stream);
@@ -316,6 +333,10 @@ OFB_API int ofb_rmsnorm(const void* x, const void* weight, void* out, int32_t ro
                         float eps, void* stream);
 /* act[b][i] = silu(gate_up[b][i]) * gate_up[b][inter + i], bf16, inter % 8 == 0. */
 OFB_API int ofb_silu_mul(const void* gate_up, void* act, int32_t batch, int32_t inter, void* stream);
+/* ss_out[t][b] = sum over columns 128t..128t+127 of x[b][c]^2 (fp32, row stride
+ * ld_batch >= rows): the ss_in of the first fused-RMSNorm projection of a step. */
+OFB_API int ofb_row_sumsq(const void* x, float* ss_out, int32_t rows, int32_t hidden, int32_t ld_batch,
+                          void* stream);
 /* Diagnostics: K6 launches write globaltimer stamps per CTA (entry, prologue done,
  * accumulator ready, cluster synced, output start, exit) into `device_buffer`
  * (uint64 [grid][8]); NULL switches tracing off. */

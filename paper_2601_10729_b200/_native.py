@@ -92,6 +92,8 @@ class OprojDesc(ctypes.Structure):
         ("symm", c_vp * 8), ("epoch", ctypes.c_uint32), ("status", c_vp), ("timeout_ns", c_i64),
         ("w_layout", c_i32), ("residual", c_vp),
         ("out_parts", c_i32), ("part_cols", c_i32 * 4), ("part_out", c_vp * 4),
+        ("ss_out", c_vp), ("ss_in", c_vp), ("ss_tiles", c_i32), ("eps", ctypes.c_float),
+        ("swiglu", c_i32), ("x_layers", c_i32),
     ]
 
 
@@ -143,6 +145,7 @@ SIGNATURES = {
     "ofb_k6_trace": (ctypes.c_int, [c_vp]),
     "ofb_rmsnorm": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i32, ctypes.c_float, c_vp]),
     "ofb_silu_mul": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_vp]),
+    "ofb_row_sumsq": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "ofb_plan_solve": (ctypes.c_int, [ctypes.POINTER(PlanProblem), ctypes.POINTER(PlanResult)]),
     "ofb_plan_last_error": (ctypes.c_char_p, []),
     "ofb_link_probe": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, ctypes.POINTER(c_f64),

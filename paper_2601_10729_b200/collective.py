@@ -144,6 +144,24 @@ def pack_weight(w: torch.Tensor) -> torch.Tensor:
     return (w.reshape(*lead, h // 128, 128, k // 64, 64).transpose(-3, -2).contiguous())
 
 
+def interleave_gate_up(w: torch.Tensor) -> torch.Tensor:
+    """[..., 2*I, K] (gate rows, then up rows) -> rows interleaved per 64 (gate
+    64t..64t+63, up 64t..64t+63, ...): each 128-row K6 tile then holds matching
+    gate and up columns, so its epilogue can emit silu(gate) * up (``swiglu``)."""
+    *lead, two_i, k = w.shape
+    i = two_i // 2
+    if two_i % 2 or i % 64:
+        raise ValueError("the gate/up rows must be 2 x a multiple of 64")
+    return w.reshape(*lead, 2, i // 64, 64, k).transpose(-4, -3).reshape(*lead, two_i, k)
+
+
+def deinterleave_gate_up(w: torch.Tensor) -> torch.Tensor:
+    """Inverse of ``interleave_gate_up``."""
+    *lead, two_i, k = w.shape
+    i = two_i // 2
+    return w.reshape(*lead, i // 64, 2, 64, k).transpose(-4, -3).reshape(*lead, two_i, k)
+
+
 class OprojAllReduce:
     """K6: ``hidden[B, H] = sum over ranks of x_r[B, K] @ W_r[H, K]^T`` per layer.
 
@@ -184,19 +202,36 @@ class OprojAllReduce:
 
     def __call__(self, x: torch.Tensor, layer: int, out: torch.Tensor | None = None,
                  stream=None, residual: torch.Tensor | None = None,
-                 parts: list | None = None) -> torch.Tensor:
+                 parts: list | None = None, ss_out: torch.Tensor | None = None,
+                 ss_in: torch.Tensor | None = None, eps: float = 1e-5,
+                 swiglu: bool = False) -> torch.Tensor:
         """``x``: bf16 [L, B, K] (or [L, B, Hq_local, 128]) - all layers' attention
-        output; layer ``layer`` is projected.  Returns bf16 [B, H].  ``residual``
-        (bf16 [B, H], may be ``out`` itself) is added before the one rounding:
-        the decoder's ``x += o_proj(attn)`` in the same kernel."""
+        output; layer ``layer`` is projected.  A 2-D ``x`` [B, K] is one input for
+        every layer (the decoder's residual stream).  Returns bf16 [B, H].
+        ``residual`` (bf16 [B, H], may be ``out`` itself) is added before the one
+        rounding: the decoder's ``x += o_proj(attn)`` in the same kernel.
+
+        Fused RMSNorm (the whole-decoder step): ``ss_out`` (fp32 [H/128, max_batch])
+        receives each hidden tile's per-row sum of squares of the final output;
+        ``ss_in`` (such a tensor from the launch that produced ``x``) scales output
+        row b by rsqrt(mean(x[b]^2) + eps), so the projection consumes
+        RMSNorm(x) with the norm weight folded into W.  ``swiglu``: W was packed
+        with ``interleave_gate_up`` and ``out`` is bf16 [B, H/2] = silu(gate) * up."""
         if not x.is_cuda or x.dtype != torch.bfloat16:
             raise ValueError("x must be a bf16 CUDA tensor (no CPU fallback)")
-        if x.shape[0] != self.layers:
-            raise ValueError("x must hold every layer: [layers, batch, ...]")
+        if x.dim() == 2:             # one input for every layer (W of `layer`)
+            x, n_layers = x.reshape(1, *x.shape), 1
+        else:
+            n_layers = self.layers
+            if x.shape[0] != self.layers:
+                raise ValueError("x must hold every layer: [layers, batch, ...] (or be [batch, k])")
         b = x.shape[1]
-        x = x.reshape(self.layers, b, -1)
+        x = x.reshape(n_layers, b, -1)
         if x.shape[2] != self.k or not x.is_contiguous():
             raise ValueError(f"x must be contiguous [layers, batch, {self.k}]")
+        if not 0 <= layer < self.layers:
+            raise ValueError("layer out of range")
+        w_layer = layer
         if parts is not None:     # column ranges into separate [B, cols] tensors (world 1)
             if out is not None or residual is not None or not 2 <= len(parts) <= 4:
                 raise ValueError("parts excludes out / residual and takes 2-4 tensors")
@@ -208,11 +243,17 @@ class OprojAllReduce:
                 if (t.dtype != torch.bfloat16 or not t.is_contiguous() or t.device != x.device
                         or t.reshape(b, -1).shape[1] % 128):
                     raise ValueError("parts must be contiguous bf16 [B, cols] tensors, cols % 128 == 0")
+        out_cols = self.hidden // 2 if swiglu else self.hidden
         if out is None and parts is None:
-            out = torch.empty((b, self.hidden), dtype=torch.bfloat16, device=x.device)
-        elif out is not None and (out.shape != (b, self.hidden) or out.dtype != torch.bfloat16 or not out.is_contiguous()
+            out = torch.empty((b, out_cols), dtype=torch.bfloat16, device=x.device)
+        elif out is not None and (out.shape != (b, out_cols) or out.dtype != torch.bfloat16 or not out.is_contiguous()
               or out.device != x.device):
-            raise ValueError(f"out must be a contiguous bf16 [{b}, {self.hidden}] tensor on {x.device}")
+            raise ValueError(f"out must be a contiguous bf16 [{b}, {out_cols}] tensor on {x.device}")
+        for name, t, rows in (("ss_out", ss_out, self.hidden // 128), ("ss_in", ss_in, None)):
+            if t is not None and (t.dtype != torch.float32 or not t.is_contiguous() or t.device != x.device
+                                  or t.dim() != 2 or t.shape[1] != self.max_batch
+                                  or (rows is not None and t.shape[0] != rows)):
+                raise ValueError(f"{name} must be a contiguous fp32 [tiles, max_batch={self.max_batch}] tensor")
         d = _native.OprojDesc()
         d.x, d.w = x.data_ptr(), self.w.data_ptr()
         d.out = out.data_ptr() if out is not None else None
@@ -221,7 +262,16 @@ class OprojAllReduce:
             for i, t in enumerate(parts):
                 d.part_cols[i] = t.reshape(b, -1).shape[1]
                 d.part_out[i] = t.data_ptr()
-        d.layers, d.layer, d.batch, d.k, d.hidden = self.layers, layer, b, self.k, self.hidden
+        d.layers, d.layer, d.batch, d.k, d.hidden = self.layers, w_layer, b, self.k, self.hidden
+        if n_layers == 1 and self.layers > 1:
+            # one x for every layer: a per-call map over [1, batch, k], W of layer w_layer
+            d.x_layers = 1
+        if ss_out is not None:
+            d.ss_out = ss_out.data_ptr()
+        if ss_in is not None:
+            d.ss_in, d.ss_tiles = ss_in.data_ptr(), ss_in.shape[0]
+        d.eps = float(eps)
+        d.swiglu = 1 if swiglu else 0
         d.workspace, d.workspace_bytes = self.ws.data_ptr(), self.ws.numel()
         d.max_batch = self.max_batch
         d.status = self._status.data_ptr()

@@ -1,11 +1,13 @@
 // Decoder glue around the data path for the whole-decoder TP step (SURVEY.md
 // 8(d) cfg4): RMSNorm of the residual stream and the SwiGLU activation.  Not
-// among the four north-star pieces - they exist so the 70B step streams every
-// weight byte with as few launches as possible (the residual add itself is
-// folded into K6, ofb_oproj_desc.residual).
+// among the four north-star pieces.  With K6 (c1="k6") both are folded into the
+// projections (the residual add, the RMSNorm's row sums of squares and 1/rms row
+// scale, and SwiGLU all live in K6's epilogues), so only ofb_row_sumsq runs, once
+// per step for the embeddings; rmsnorm / silu_mul serve the cuBLAS + NCCL arm.
 //
-//   rmsnorm:  a[b] = x[b] / sqrt(mean(x[b]^2) + eps) * w        (one CTA per row)
-//   silu_mul: act[b, i] = silu(gu[b, i]) * gu[b, inter + i]      (grid-stride)
+//   rmsnorm:    a[b] = x[b] / sqrt(mean(x[b]^2) + eps) * w        (one CTA per row)
+//   silu_mul:   act[b, i] = silu(gu[b, i]) * gu[b, inter + i]      (grid-stride)
+//   row_sumsq:  ss[t][b] = sum of x[b][128t .. 128t+127]^2          (one CTA per tile)
 #include "common.cuh"
 
 #include "../../include/orbitflow_b200.h"
@@ -101,6 +103,24 @@ __global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloa
   }
 }
 
+// ss[t][b] = sum of x[b][128t .. 128t+127]^2: one CTA per 128-column tile, one
+// warp per row (4 columns per lane, a fixed shuffle order).
+__global__ void row_sumsq_kernel(const __nv_bfloat16* __restrict__ x, float* __restrict__ ss, int rows,
+                                 int hidden, int ld_batch) {
+  pdl_wait();
+  pdl_trigger();
+  const int t = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int b = warp; b < rows; b += blockDim.x >> 5) {
+    const uint2 u = *reinterpret_cast<const uint2*>(x + static_cast<size_t>(b) * hidden + t * 128 + lane * 4);
+    const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    float s = f0.x * f0.x + f0.y * f0.y + f1.x * f1.x + f1.y * f1.y;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) ss[static_cast<size_t>(t) * ld_batch + b] = s;
+  }
+}
+
 // Launch with programmatic stream serialization (unless OFB_PDL=0): the glue
 // kernels wait for their predecessor before reading anything and release their
 // dependent at once, so the next K6 requests its weight ring while they run.
@@ -139,6 +159,17 @@ int ofb_rmsnorm(const void* x, const void* weight, void* out, int32_t rows, int3
                        : per <= 2 ? launch_pdl(rmsnorm_kernel<2>, rows, kNormThreads, s, xp, wp, op, hidden, eps)
                                   : launch_pdl(rmsnorm_kernel<4>, rows, kNormThreads, s, xp, wp, op, hidden, eps);
   return e == cudaSuccess ? 0 : report_cuda(e, "rmsnorm_kernel launch");
+}
+
+int ofb_row_sumsq(const void* x, float* ss_out, int32_t rows, int32_t hidden, int32_t ld_batch,
+                  void* stream) {
+  using namespace ofb;
+  if (!x || !ss_out || rows < 0 || ld_batch < rows || hidden <= 0 || hidden % 128)
+    return report_error(-1, "ofb_row_sumsq: bad arguments (hidden % 128, ld_batch >= rows)");
+  if (rows == 0) return 0;
+  const cudaError_t e = launch_pdl(row_sumsq_kernel, hidden / 128, 256, static_cast<cudaStream_t>(stream),
+                                   static_cast<const __nv_bfloat16*>(x), ss_out, rows, hidden, ld_batch);
+  return e == cudaSuccess ? 0 : report_cuda(e, "row_sumsq_kernel launch");
 }
 
 int ofb_silu_mul(const void* gate_up, void* act, int32_t batch, int32_t inter, void* stream) {

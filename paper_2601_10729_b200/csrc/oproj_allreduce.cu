@@ -64,6 +64,12 @@ struct OprojArgs {
   unsigned long long* trace;   // diagnostics (ofb_k6_trace): per CTA stamps, or null
   const __nv_bfloat16* residual;   // added before the final rounding, or null (may alias out)
   int parts;                       // > 1: column ranges written to separate tensors (world 1)
+  float* ss_out;                   // fp32 [tiles][max_batch]: sum over the tile's columns of out^2, or null
+  const float* ss_in;              // fp32 [ss_tiles][max_batch]: a producer's ss_out (fused RMSNorm), or null
+  int ss_tiles;
+  float eps;
+  int swiglu;                      // 1: rows interleaved gate 64 / up 64; out [batch][hidden/2] = silu(g) * u
+  int x_layer;                     // x's layer coordinate (0 when one x serves every layer)
   int part_lo[5];                  // first column of range i (part_lo[parts] = hidden)
   __nv_bfloat16* part_out[4];
 };
@@ -169,6 +175,17 @@ __device__ __forceinline__ long long globaltimer() {
   return t;
 }
 
+__device__ __forceinline__ float sumsq_bf16x8(uint4 u) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    s += f.x * f.x + f.y * f.y;
+  }
+  return s;
+}
+
 __device__ __forceinline__ void add_bf16x8(float* acc, uint4 u) {
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
@@ -248,14 +265,14 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
     // TMA producer: the first stages' W loads are in flight (above)
     pdl_wait();
     for (int i = 0; i < pre; ++i)
-      tma_load_3d(smem + i * stage_bytes + stage_w, &xmap, &full_bar[i], (c0 + i) * kChunkK, 0, a.layer);
+      tma_load_3d(smem + i * stage_bytes + stage_w, &xmap, &full_bar[i], (c0 + i) * kChunkK, 0, a.x_layer);
     for (int i = pre; i < nchunks; ++i) {
       const int s = i % a.stages, round = i / a.stages;
       mbar_wait(&empty_bar[s], (round - 1) & 1);
       uint8_t* sw = smem + s * stage_bytes;
       mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
       tma_load_4d(sw, &wmap, &full_bar[s], 0, 0, c0 + i, a.layer * a.tiles + tile);
-      tma_load_3d(sw + stage_w, &xmap, &full_bar[s], (c0 + i) * kChunkK, 0, a.layer);
+      tma_load_3d(sw + stage_w, &xmap, &full_bar[s], (c0 + i) * kChunkK, 0, a.x_layer);
     }
   } else if (warp == 1 && lane == 0) {
     // MMA issuer: D[128 x npad] (TMEM) += W_tile[128 x 64] . X[npad x 64]^T per stage
@@ -276,6 +293,20 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
   __syncwarp();
 
   // ---- epilogue (row m = warp*32 + lane of the tile)
+  // Fused RMSNorm of the input rows (ss_in): the producer of x left, per hidden
+  // tile, the sum of squares of each row; summed here in tile order while the
+  // MMAs still run.  out[b] = (x[b] . W'^T) * rsqrt(mean(x[b]^2) + eps), the
+  // norm weight having been folded into W' (pack time).
+  __shared__ float rsc[256];
+  if (a.ss_in && split == 0) {
+    pdl_wait();
+    for (int b = threadIdx.x; b < a.batch; b += kThreads) {
+      float s = 0.f;
+      for (int t = 0; t < a.ss_tiles; ++t) s += __ldcg(a.ss_in + static_cast<size_t>(t) * a.max_batch + b);
+      rsc[b] = rsqrtf(s / static_cast<float>(a.ss_tiles * kTileM) + a.eps);
+    }
+    if (a.splits == 1) __syncthreads();   // else the cluster barrier below publishes rsc
+  }
   mbar_wait(&acc_bar, 0);
   if (tr) tr[2] = globaltimer();
   tc_fence_after();
@@ -326,6 +357,11 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
 #pragma unroll
       for (int j = 0; j < 32; ++j) acc[j] += src[j * kTileM];
     }
+    if (a.ss_in) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (c * 32 + j < a.batch) acc[j] *= rsc[c * 32 + j];
+    }
     if (a.world == 1 && a.residual) {   // x += o_proj(attn): one rounding of x + sum
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
@@ -344,6 +380,45 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
   const int nvec = a.batch * (kTileM / 8);     // 16-byte vectors of the [batch][128] tile
   const uint4* s4 = reinterpret_cast<const uint4*>(stg);
   if (tr) tr[4] = globaltimer();
+  if (a.world == 1 && a.ss_out) {
+    // per batch row, the sum of squares of this tile's final (rounded) values: one
+    // warp per row, fixed order - the next projection's fused RMSNorm
+    for (int b = warp; b < a.batch; b += kThreads / 32) {
+      const uint2 u = reinterpret_cast<const uint2*>(stg + static_cast<size_t>(b) * kTileM)[lane];
+      const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+      const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+      float s = f0.x * f0.x + f0.y * f0.y + f1.x * f1.x + f1.y * f1.y;
+#pragma unroll
+      for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      if (lane == 0) a.ss_out[static_cast<size_t>(tile) * a.max_batch + b] = s;
+    }
+  }
+  if (a.world == 1 && a.swiglu) {
+    // SwiGLU: tile rows 0-63 are gate columns 64*tile.., rows 64-127 the matching
+    // up columns; act[b][64*tile + i] = silu(gate) * up from the bf16-rounded values
+    const int inter = a.hidden / 2;
+    for (int i = threadIdx.x; i < a.batch * 8; i += kThreads) {
+      const int b = i >> 3, q = i & 7;
+      const uint4 gv = s4[b * 16 + q], uv = s4[b * 16 + 8 + q];
+      const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
+      const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&uv);
+      float o[8];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 g = __bfloat1622float2(g2[e]), u = __bfloat1622float2(u2[e]);
+        o[2 * e] = g.x / (1.f + __expf(-g.x)) * u.x;
+        o[2 * e + 1] = g.y / (1.f + __expf(-g.y)) * u.y;
+      }
+      uint4 pk;
+      pk.x = pack_bf16(o[0], o[1]);
+      pk.y = pack_bf16(o[2], o[3]);
+      pk.z = pack_bf16(o[4], o[5]);
+      pk.w = pack_bf16(o[6], o[7]);
+      *reinterpret_cast<uint4*>(a.out + static_cast<size_t>(b) * inter + tile * 64 + q * 8) = pk;
+    }
+    if (tr) tr[5] = globaltimer();
+    return;
+  }
   if (a.world == 1) {
     // the column range (tensor) this tile belongs to: one lookup per CTA
     __nv_bfloat16* dst_base = a.out;
@@ -392,7 +467,8 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
   const __nv_bfloat16* inbox = reinterpret_cast<const __nv_bfloat16*>(a.symm[a.rank]) +
                                static_cast<size_t>(p) * a.world * src_stride + tile * slot;
   constexpr int kUnroll = 4;   // vectors per thread whose loads are all issued before any store
-  for (int i0 = threadIdx.x; i0 < nvec; i0 += kThreads * kUnroll) {
+  // warp-uniform trip count (the ss_out shuffles need every lane)
+  for (int i0 = threadIdx.x; i0 - lane < nvec; i0 += kThreads * kUnroll) {
     float acc[kUnroll][8];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u)
@@ -423,14 +499,22 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const int i = i0 + u * kThreads;
-      if (i >= nvec) break;
       uint4 o;
       o.x = pack_bf16(acc[u][0], acc[u][1]);
       o.y = pack_bf16(acc[u][2], acc[u][3]);
       o.z = pack_bf16(acc[u][4], acc[u][5]);
       o.w = pack_bf16(acc[u][6], acc[u][7]);
       const int b = i >> 4, q = i & 15;
-      *reinterpret_cast<uint4*>(a.out + static_cast<size_t>(b) * a.hidden + tile * kTileM + q * 8) = o;
+      if (i < nvec)
+        *reinterpret_cast<uint4*>(a.out + static_cast<size_t>(b) * a.hidden + tile * kTileM + q * 8) = o;
+      if (a.ss_out) {
+        // the 16 vectors of row b sit in 16 consecutive lanes: reduce them in a
+        // fixed order (identical on every rank, like the sum itself)
+        float s = i < nvec ? sumsq_bf16x8(o) : 0.f;
+#pragma unroll
+        for (int off = 8; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (i < nvec && q == 0) a.ss_out[static_cast<size_t>(tile) * a.max_batch + b] = s;
+      }
     }
   }
 }
@@ -487,7 +571,7 @@ size_t flags_bytes(int world, int hidden) {
 struct MapKey {
   const void* x;
   const void* w;
-  int layers, batch, k, hidden, npad, w_layout;
+  int layers, batch, k, hidden, npad, w_layout, x_layers;
   CUtensorMap xmap, wmap;
 };
 unsigned long long* g_k6_trace = nullptr;
@@ -498,16 +582,17 @@ int get_maps(const ofb_oproj_desc* d, int npad, CUtensorMap* xmap, CUtensorMap* 
   std::lock_guard<std::mutex> lock(g_map_mu);
   for (auto& e : g_map_cache)
     if (e.x == d->x && e.w == d->w && e.layers == d->layers && e.batch == d->batch &&
-        e.k == d->k && e.hidden == d->hidden && e.npad == npad && e.w_layout == d->w_layout) {
+        e.k == d->k && e.hidden == d->hidden && e.npad == npad && e.w_layout == d->w_layout &&
+        e.x_layers == d->x_layers) {
       *xmap = e.xmap;
       *wmap = e.wmap;
       return 0;
     }
-  MapKey e{d->x, d->w, d->layers, d->batch, d->k, d->hidden, npad, d->w_layout, {}, {}};
+  MapKey e{d->x, d->w, d->layers, d->batch, d->k, d->hidden, npad, d->w_layout, d->x_layers, {}, {}};
   const uint64_t row = static_cast<uint64_t>(d->k) * 2;
   {  // X: [layers][batch][k]; box 64 x npad x 1 (rows past the batch read as zero)
     uint64_t dims[3] = {static_cast<uint64_t>(d->k), static_cast<uint64_t>(d->batch),
-                        static_cast<uint64_t>(d->layers)};
+                        static_cast<uint64_t>(d->x_layers == 1 ? 1 : d->layers)};
     uint64_t strides[2] = {row, row * d->batch};
     uint32_t box[3] = {static_cast<uint32_t>(kChunkK), static_cast<uint32_t>(npad), 1};
     int rc = encode_bf16_map(&e.xmap, const_cast<void*>(d->x), 3, dims, strides, box);
@@ -702,6 +787,18 @@ int ofb_oproj_allreduce(const ofb_oproj_desc* d, void* stream) {
     if (lo != d->hidden) return report_error(-1, "ofb_oproj_allreduce: part_cols must sum to hidden");
   }
   a.flags_off = static_cast<long long>((inbox_bytes(d->world, d->max_batch, d->hidden) + 255) / 256 * 256);
+  a.ss_out = d->ss_out;
+  a.ss_in = d->ss_in;
+  a.ss_tiles = d->ss_tiles;
+  a.eps = d->eps;
+  a.swiglu = d->swiglu;
+  if (d->x_layers != 0 && d->x_layers != 1) return report_error(-1, "ofb_oproj_allreduce: x_layers must be 0 or 1");
+  a.x_layer = d->x_layers == 1 ? 0 : d->layer;
+  if (d->ss_in && (d->world != 1 || d->ss_tiles < 1 || !(d->eps >= 0.f)))
+    return report_error(-1, "ofb_oproj_allreduce: ss_in needs world 1, ss_tiles >= 1 and eps >= 0");
+  if (d->swiglu && (d->world != 1 || d->residual || a.parts || d->ss_out || !d->out))
+    return report_error(-1, "ofb_oproj_allreduce: swiglu needs world 1, an out tensor, no residual / parts / ss_out");
+  if (d->ss_out && a.parts) return report_error(-1, "ofb_oproj_allreduce: ss_out excludes out_parts");
 
   const size_t smem = static_cast<size_t>(a.stages) * stage_bytes + red_bytes(splits, npad) + 1024;
   {  // the dynamic-smem opt-in is per device: set it once for each device used

@@ -189,7 +189,7 @@ class TensorParallelLlama:
     """One rank of a whole Llama decoder step, KV-head sharded.
 
     Per layer, on one stream: input RMSNorm -> q / k / v projections of this
-    rank's heads (cuBLAS) -> K3 append of the fresh token + K2 fetch wait + K1
+    rank's heads -> K3 append of the fresh token + K2 fetch wait + K1
     attention (the native step split per layer, ``append_per_layer``: k_new /
     v_new of layer l only exist once layer l-1 finished) -> o-projection with
     its all-reduce (C1) -> residual -> RMSNorm -> gate / up projection (cuBLAS)
@@ -197,9 +197,14 @@ class TensorParallelLlama:
     weight byte of the 70B shard is streamed from HBM each step (137 GB / TP),
     and the step time is the real decoder's, not attention alone.
 
-    ``c1="k6"``: both reductions are K6 (``collective.OprojAllReduce``: tcgen05
-    projection fused with the one-shot all-reduce over IPC peer memory; the
-    down projection has the same shape class).  ``c1="nccl"``: cuBLAS
+    ``c1="k6"``: every projection is K6 (``collective.OprojAllReduce``: tcgen05
+    projection, the o / down ones fused with the one-shot all-reduce over IPC
+    peer memory) and the glue is folded into it: each RMSNorm becomes the
+    producing K6's per-tile row sum of squares (``ss_out``, after the residual
+    add) plus a 1/rms row scale in the consuming K6's epilogue (``ss_in``; the
+    norm weight is folded into its packed W), and SwiGLU is the gate/up K6's
+    epilogue (gate/up rows interleaved per 64) - 3 launches fewer per layer.
+    ``c1="nccl"``: cuBLAS
     projection + ``torch.distributed.all_reduce`` (NCCL over NVLink) - the
     unfused baseline the north star names.  With world 1 (a
     TP-N shard emulated on one GPU) there is no exchange in either arm.
@@ -227,17 +232,27 @@ class TensorParallelLlama:
         g = torch.Generator(device=dev)
         g.manual_seed(7001 + 131 * seed + shard.rank)
 
-        from .collective import pack_weight
+        from .collective import interleave_gate_up, pack_weight
 
-        def rand(shape, fan_in, packed=False):
+        self.norm = torch.ones((2, hidden), dtype=torch.bfloat16, device=dev)
+
+        def rand(shape, fan_in, packed=False, norm=None, gate_up=False):
             """Random bf16 layers, generated one layer at a time (no full-size
-            temporaries: the 70B shard fills most of HBM); ``packed``: K6 layout."""
+            temporaries: the 70B shard fills most of HBM); ``packed``: K6 layout,
+            with ``norm`` (the input RMSNorm weight) folded into the columns and
+            ``gate_up`` rows interleaved for the SwiGLU epilogue."""
             L_, h, k = shape
             out = torch.empty((L_, h // 128, k // 64, 128, 64) if packed else shape,
                               dtype=torch.bfloat16, device=dev)
             for l in range(L_):
                 w = (torch.randn((h, k), generator=g, device=dev) * fan_in ** -0.5).to(torch.bfloat16)
-                out[l] = pack_weight(w) if packed else w
+                if packed:
+                    if norm is not None:
+                        w = (w.float() * norm.float()[None, :]).to(torch.bfloat16)
+                    if gate_up:
+                        w = interleave_gate_up(w)
+                    w = pack_weight(w)
+                out[l] = w
             return out
 
         qkv_rows = (hq + 2 * hkv) * 128
@@ -245,14 +260,13 @@ class TensorParallelLlama:
         # with K6 every projection runs on it (the column-parallel q/k/v and
         # gate/up ones with world 1: no exchange); the NCCL arm is the cuBLAS
         # baseline throughout
-        self.w_qkv = rand((L, qkv_rows, hidden), hidden, packed)
-        self.w_gu = rand((L, 2 * self.inter, hidden), hidden, packed)
+        self.w_qkv = rand((L, qkv_rows, hidden), hidden, packed, norm=self.norm[0])
+        self.w_gu = rand((L, 2 * self.inter, hidden), hidden, packed, norm=self.norm[1], gate_up=True)
         if packed:
             self.qkv_proj = OprojAllReduce(self.w_qkv, max_batch)
             self.gu_proj = OprojAllReduce(self.w_gu, max_batch)
         w_o = rand((L, hidden, hq * 128), shard.num_q_heads * 128, packed)
         w_d = rand((L, hidden, self.inter), intermediate, packed)
-        self.norm = torch.ones((2, hidden), dtype=torch.bfloat16, device=dev)
         self.symm = None
         if c1 == "k6":
             if self.world > 1:
@@ -271,6 +285,8 @@ class TensorParallelLlama:
         """Layer ``l``'s weights in ``nn.Linear`` layout [out, in] (test / reference use)."""
         nq, nk = self.shard.local_q * 128, self.shard.local_kv * 128
 
+        from .collective import deinterleave_gate_up
+
         def unpack(t):
             if t.dim() == 2:
                 return t
@@ -278,6 +294,8 @@ class TensorParallelLlama:
             return t.permute(0, 2, 1, 3).reshape(tiles * 128, chunks * 64)
 
         w, gu = unpack(self.w_qkv[l]), unpack(self.w_gu[l])
+        if self.c1 == "k6":   # packed: gate/up interleaved, norm weights folded in (unit here)
+            gu = deinterleave_gate_up(gu)
         o = unpack(self.oproj.w[l]) if self.c1 == "k6" else self.w_o[l]
         d = unpack(self.down.w[l]) if self.c1 == "k6" else self.w_d[l]
         return {"q": w[:nq], "k": w[nq:nq + nk], "v": w[nq + nk:], "o": o,
@@ -300,15 +318,18 @@ class TensorParallelLlama:
                           "v_new": mk(L, B, hkv, 128), "act": mk(L, B, self.inter),
                           "h": mk(B, self.hidden), "x": [mk(B, self.hidden), mk(B, self.hidden)],
                           "a": mk(L, B, self.hidden), "a2": mk(L, B, self.hidden),
-                          "gu": mk(B, 2 * self.inter)}
+                          "gu": mk(B, 2 * self.inter),
+                          # per hidden tile, per row: sum of x^2 (the fused RMSNorms)
+                          "ss": torch.empty((self.hidden // 128, self.max_batch), dtype=torch.float32,
+                                            device=dev)}
         return self._bufs
 
-    def _reduce(self, proj, w, x_all, l, x, h, stream):
+    def _reduce(self, proj, w, x_all, l, x, h, stream, ss=None):
         """x += sum over ranks of x_all[l] @ w[l]^T (C1).  K6 folds the residual
-        add into its epilogue; the NCCL arm projects into ``h``, all-reduces it
-        and adds."""
+        add into its epilogue (and leaves the new x's row sums of squares in
+        ``ss``); the NCCL arm projects into ``h``, all-reduces it and adds."""
         if self.c1 == "k6":
-            proj(x_all, l, out=x, stream=stream, residual=x)
+            proj(x_all, l, out=x, stream=stream, residual=x, ss_out=ss)
             return
         torch.matmul(x_all[l].reshape(h.shape[0], -1), w[l].t(), out=h)
         if self.world > 1:
@@ -350,31 +371,38 @@ class TensorParallelLlama:
         nq, nk = self.shard.local_q * 128, self.shard.local_kv * 128
         a_all, a2_all, gu = bufs["a"], bufs["a2"], bufs["gu"]
         k6 = self.c1 == "k6"
+        ss = bufs["ss"]
+        if k6:   # the first layer's fused RMSNorm: row sums of squares of the embeddings
+            from . import _native
+
+            _native.check(_native.load().ofb_row_sumsq(x.data_ptr(), ss.data_ptr(), B, self.hidden,
+                                                       self.max_batch, stream.cuda_stream), "ofb_row_sumsq")
         ex.runtime.step_begin(desc, stream)
         try:
             for l in range(L):
                 a = a_all[l]
-                self._rmsnorm(x, self.norm[0], a, stream)
-                if k6:     # q / k / v of this rank's heads in one launch, into their buffers
-                    self.qkv_proj(a_all, l, stream=stream,
+                if k6:     # RMSNorm(x) . W_qkv^T for this rank's heads in one launch, into their buffers
+                    self.qkv_proj(x, l, stream=stream, ss_in=ss, eps=self.eps,
                                   parts=[q[l].view(B, nq), kn[l].view(B, nk), vn[l].view(B, nk)])
                 else:
+                    self._rmsnorm(x, self.norm[0], a, stream)
                     w = self.w_qkv[l]
                     torch.matmul(a, w[:nq].t(), out=q[l].view(B, nq))
                     torch.matmul(a, w[nq:nq + nk].t(), out=kn[l].view(B, nk))
                     torch.matmul(a, w[nq + nk:].t(), out=vn[l].view(B, nk))
                 ex.runtime.step_layers(1)                    # K3 + K2 wait + K1 of layer l
                 self._reduce(getattr(self, "oproj", None), getattr(self, "w_o", None), out, l, x, h,
-                             stream)                         # x += o_proj(attn) (C1)
-                a2 = a2_all[l]
-                self._rmsnorm(x, self.norm[1], a2, stream)
-                if k6:
-                    self.gu_proj(a2_all, l, out=gu, stream=stream)
+                             stream, ss)                     # x += o_proj(attn) (C1)
+                if k6:     # act = silu(gate) * up of RMSNorm(x) . W_gu^T, one launch
+                    self.gu_proj(x, l, out=bufs["act"][l], stream=stream, ss_in=ss, eps=self.eps,
+                                 swiglu=True)
                 else:
+                    a2 = a2_all[l]
+                    self._rmsnorm(x, self.norm[1], a2, stream)
                     torch.matmul(a2, self.w_gu[l].t(), out=gu)
-                self._silu_mul(gu, bufs["act"][l], stream)
+                    self._silu_mul(gu, bufs["act"][l], stream)
                 self._reduce(getattr(self, "down", None), getattr(self, "w_d", None), bufs["act"],
-                             l, x, h, stream)                # x += down(act) (C1)
+                             l, x, h, stream, ss)            # x += down(act) (C1)
         except BaseException:
             ex.runtime.step_abort()
             raise

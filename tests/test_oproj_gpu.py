@@ -254,3 +254,104 @@ def test_fused_residual_adds_before_the_rounding():
     op(xs[0].to(dev), 0, out=x_res, residual=x_res)       # in place: x += proj
     torch.cuda.synchronize()
     torch.testing.assert_close(x_res.float(), want, rtol=RTOL, atol=ATOL)
+
+
+def _rms(x, eps=1e-5):
+    return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + eps)
+
+
+def _tile_sumsq(y, max_batch):
+    """fp32 [H/128, max_batch]: per 128-column tile, each row's sum of squares."""
+    b, h = y.shape
+    out = torch.zeros((h // 128, max_batch), dtype=torch.float32)
+    out[:, :b] = y.float().pow(2).reshape(b, h // 128, 128).sum(-1).T
+    return out
+
+
+def test_fused_rmsnorm_ss_out_and_ss_in():
+    """A producer K6 (residual add) leaves each tile's row sums of squares of its
+    final output; a consumer K6 fed a 2-D x (one input for every layer) and that
+    ss scales its rows by rsqrt(mean(x^2)+eps) - RMSNorm(x) . W^T; the first
+    layer's ss comes from ofb_row_sumsq."""
+    from paper_2601_10729_b200 import _native
+    from paper_2601_10729_b200.collective import OprojAllReduce
+
+    dev = torch.device("cuda:0")
+    b, k, h, mb = 13, 512, 1024, 16
+    xs, ws = _inputs(1, 2, b, k, h, seed=21)
+    prod = OprojAllReduce(ws[0].to(dev), max_batch=mb)
+    res = torch.randn((b, h), generator=torch.Generator().manual_seed(8)).to(torch.bfloat16)
+    x = res.to(dev).clone()
+    ss = torch.zeros((h // 128, mb), dtype=torch.float32, device=dev)
+    prod(xs[0].to(dev), 1, out=x, residual=x, ss_out=ss)
+    torch.cuda.synchronize()
+    torch.testing.assert_close(ss.cpu(), _tile_sumsq(x.cpu(), mb), rtol=1e-5, atol=1e-4)
+    # ofb_row_sumsq gives the same layout for an arbitrary x
+    ss2 = torch.zeros_like(ss)
+    _native.check(_native.load().ofb_row_sumsq(x.data_ptr(), ss2.data_ptr(), b, h, mb, None), "row_sumsq")
+    torch.cuda.synchronize()
+    torch.testing.assert_close(ss2.cpu(), ss.cpu(), rtol=1e-6, atol=1e-5)
+    # consumer: 3 layers of W [512, h], one x for every layer
+    w_c = (torch.randn((3, 512, h), generator=torch.Generator().manual_seed(9)) * h ** -0.5).to(torch.bfloat16)
+    cons = OprojAllReduce(w_c.to(dev), max_batch=mb)
+    for layer in (0, 2):
+        got = cons(x, layer, ss_in=ss, eps=1e-5)
+        torch.cuda.synchronize()
+        want = _rms(x.float().cpu()) @ w_c[layer].float().T
+        torch.testing.assert_close(got.float().cpu(), want, rtol=RTOL, atol=ATOL)
+
+
+def test_swiglu_epilogue():
+    """Gate/up rows interleaved per 64: the K6 epilogue emits silu(gate) * up of
+    the rounded projections (with the fused RMSNorm row scale)."""
+    import torch.nn.functional as F
+
+    from paper_2601_10729_b200.collective import OprojAllReduce, deinterleave_gate_up, interleave_gate_up
+
+    dev = torch.device("cuda:0")
+    b, k, inter, mb = 9, 256, 384, 16
+    g = torch.Generator().manual_seed(31)
+    w_gu = (torch.randn((2, 2 * inter, k), generator=g) * k ** -0.5).to(torch.bfloat16)
+    assert torch.equal(deinterleave_gate_up(interleave_gate_up(w_gu)), w_gu)
+    op = OprojAllReduce(interleave_gate_up(w_gu).to(dev), max_batch=mb)
+    x = torch.randn((b, k), generator=g).to(torch.bfloat16)
+    ss = torch.zeros((k // 128, mb), dtype=torch.float32)
+    ss[:, :b] = x.float().pow(2).reshape(b, k // 128, 128).sum(-1).T
+    act = op(x.to(dev), 1, ss_in=ss.to(dev), eps=1e-5, swiglu=True)
+    torch.cuda.synchronize()
+    a = _rms(x.float())
+    gu = (a @ w_gu[1].float().T).to(torch.bfloat16).float()
+    want = F.silu(gu[:, :inter]) * gu[:, inter:]
+    assert act.shape == (b, inter)
+    torch.testing.assert_close(act.float().cpu(), want, rtol=RTOL, atol=ATOL)
+
+
+def test_exchange_leaves_identical_row_sums_on_every_rank():
+    """With the all-reduce (world 2, emulated), ss_out is computed from the
+    reduced output in a fixed order: identical on both ranks and equal to the
+    output's tile sums."""
+    from paper_2601_10729_b200.collective import OprojAllReduce, SymmetricBuffers
+
+    dev = torch.device("cuda:0")
+    world, b, k, h = 2, 11, 256, 1024
+    bufs = SymmetricBuffers.emulated(world, b, h, device=dev)
+    try:
+        xs, ws = _inputs(world, 1, b, k, h, seed=55)
+        ops = [OprojAllReduce(ws[r].to(dev), b, bufs[r]) for r in range(world)]
+        res = torch.randn((b, h), generator=torch.Generator().manual_seed(4)).to(torch.bfloat16).to(dev)
+        outs = [res.clone() for _ in range(world)]
+        sss = [torch.zeros((h // 128, b), dtype=torch.float32, device=dev) for _ in range(world)]
+        streams = [torch.cuda.Stream(dev) for _ in range(world)]
+        torch.cuda.synchronize()
+        for r in range(world):
+            with torch.cuda.stream(streams[r]):
+                ops[r](xs[r].to(dev), 0, out=outs[r], residual=outs[r], ss_out=sss[r])
+        torch.cuda.synchronize()
+        for buf in bufs:
+            buf.check()
+        assert torch.equal(outs[0], outs[1]) and torch.equal(sss[0], sss[1])
+        torch.testing.assert_close(sss[0].cpu(), _tile_sumsq(outs[0].cpu(), b), rtol=1e-5, atol=1e-4)
+        want = _want(xs, ws, 0) + res.float().cpu()
+        torch.testing.assert_close(outs[0].float().cpu(), want, rtol=RTOL, atol=ATOL)
+    finally:
+        bufs[0].close()
