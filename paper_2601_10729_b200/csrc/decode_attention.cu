@@ -53,6 +53,7 @@ struct AttnArgs {
   int blocks_per_split, max_splits;
   float scale_log2;
   int kv_ready;                 // 1: KV complete before the PDL wait (see the stream kernel)
+  int defer_combine;            // 1: multi-split pairs stop after their partials (attn_combine_kernel)
   unsigned long long* trace;    // diagnostics (ofb_k1_trace): kSplitTraceSlots stamps per CTA
   int trace_ctas;               // capacity of `trace` in CTAs
 };
@@ -371,7 +372,7 @@ __device__ __forceinline__ void paged_gqa_decode_body(const CUtensorMap& kv_map,
     }
   }
   if (tr && tid == 0) tr[4] = split_gtimer();
-  if (single) {
+  if (single || a.defer_combine) {
     if (tr && tid == 0) tr[6] = split_gtimer();
     return;
   }
@@ -468,6 +469,84 @@ __device__ __forceinline__ void paged_gqa_decode_body(const CUtensorMap& kv_map,
   }
   if (tid == 0) a.counters[req * a.hkv + kvh] = 0;  // re-arm for the next launch
   if (tr && tid == 0) tr[6] = split_gtimer();
+}
+
+// Deferred combine (variant "split2"): a second, programmatically launched
+// kernel merges the splits of every (request, KV head, query row) - one CTA each,
+// the splits dealt to 4 thread groups (one row's 32 dim-quads per group) that
+// stream lse + partial with an online rescale and meet in smem.  Replaces the
+// split kernel's ticket (~0.9 us) and its one-CTA-per-pair serial combine.
+__global__ void __launch_bounds__(128) attn_combine_kernel(const AttnArgs a) {
+  // release the next kernel at once (the next layer's K1 may stream its KV
+  // while this waits; it cannot touch q / out / the workspace before its own
+  // wait, which follows this kernel's completion), then wait for every partial
+  pdl_trigger();
+  pdl_wait();
+  const int row = blockIdx.x, kvh = blockIdx.y, req = blockIdx.z;
+  const int seq = a.seq_lens[req];
+  const int nblk = (seq + kBlockTokens - 1) / kBlockTokens;
+  const int nsplit = (nblk + a.blocks_per_split - 1) / a.blocks_per_split;
+  if (nsplit <= 1) return;               // written directly by the split kernel
+  const int q4 = threadIdx.x & 31, part = threadIdx.x >> 5;
+  const size_t qrow = (size_t)req * a.hq + kvh * a.group + row;
+  const float4* src = reinterpret_cast<const float4*>(a.ws_o + qrow * a.max_splits * kHeadDim) + q4;
+  const float* lse = a.ws_lse + qrow * a.max_splits;
+  const float NEG_INF = -INFINITY;
+  float M = NEG_INF, S = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int s0 = part; s0 < nsplit; s0 += 4 * 16) {
+    float lv[16];
+    float4 v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int s2 = s0 + 4 * u;
+      const bool ok = s2 < nsplit;
+      lv[u] = ok ? __ldcg(lse + s2) : NEG_INF;
+      v[u] = ok ? __ldcg(src + (size_t)s2 * (kHeadDim / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float mr = lv[0];
+#pragma unroll
+    for (int u = 1; u < 16; ++u) mr = fmaxf(mr, lv[u]);
+    const float Mn = fmaxf(M, mr);
+    const float sc = M > NEG_INF ? fast_exp2(M - Mn) : 0.f;
+    S *= sc;
+    acc = make_float4(acc.x * sc, acc.y * sc, acc.z * sc, acc.w * sc);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const float w = lv[u] > NEG_INF ? fast_exp2(lv[u] - Mn) : 0.f;
+      S += w;
+      acc.x += w * v[u].x;
+      acc.y += w * v[u].y;
+      acc.z += w * v[u].z;
+      acc.w += w * v[u].w;
+    }
+    M = Mn;
+  }
+  __shared__ float sm_m[4][32], sm_s[4][32];
+  __shared__ float4 sm_o[4][32];
+  sm_m[part][q4] = M;
+  sm_s[part][q4] = S;
+  sm_o[part][q4] = acc;
+  __syncthreads();
+  if (part != 0) return;
+  float Mt = NEG_INF;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) Mt = fmaxf(Mt, sm_m[p][q4]);
+  float St = 0.f;
+  float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {           // part order: deterministic
+    const float w = sm_m[p][q4] > NEG_INF ? fast_exp2(sm_m[p][q4] - Mt) : 0.f;
+    St += w * sm_s[p][q4];
+    o.x += w * sm_o[p][q4].x;
+    o.y += w * sm_o[p][q4].y;
+    o.z += w * sm_o[p][q4].z;
+    o.w += w * sm_o[p][q4].w;
+  }
+  const float r = St > 0.f ? 1.f / St : 0.f;
+  __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(a.out + qrow * kHeadDim + q4 * 4);
+  dst[0] = __floats2bfloat162_rn(o.x * r, o.y * r);
+  dst[1] = __floats2bfloat162_rn(o.z * r, o.w * r);
 }
 
 // The two instantiations, each with its own launch bounds (narrow: two CTAs per SM).
@@ -595,6 +674,7 @@ static int k1_variant() {
                    : std::strcmp(v, "split") == 0   ? 1
                    : std::strcmp(v, "stream") == 0  ? 0
                    : std::strcmp(v, "cluster") == 0 ? 3
+                   : std::strcmp(v, "split2") == 0  ? 4
                                                     : 2;
   }
   return g_k1_variant;
@@ -632,9 +712,23 @@ bool cluster_preferred(int batch, int hq, int hkv, int max_seq_len) {
   return (pairs <= 4 && bps <= 40) || (pairs <= 8 && nblk <= 64);
 }
 
-static int pick_variant(int batch, int hq, int hkv, int max_seq_len) {
+// Auto.  A standalone launch (the public entry point, which waits for its
+// predecessor before streaming) with a one-wave, multi-split grid over <= 16
+// pairs uses split2: the separate combine kernel beat both the last-CTA combine
+// and the cluster kernel on every such shape (profiles/r02_k1_split2.md).  Inside a
+// step one kernel per layer is kept (split / cluster): the later layers stream
+// their KV before the PDL wait, and a combine kernel between two layers cost
+// 0.5 us per layer there (the next cluster K1 places its clusters around it).
+static int pick_variant(int batch, int hq, int hkv, int max_seq_len, bool standalone = false) {
   const int v = k1_variant();
   if (v != 2) return v;
+  if (standalone && attn_init_once() == cudaSuccess && hkv > 0 && hq % hkv == 0) {
+    const AttnPlan p = plan_splits(batch, hq, hkv, max_seq_len, g_num_sms, g_attn_occupancy);
+    const long ctas = (long)p.max_splits * hkv * batch;
+    // <= 16 (request, KV head) pairs: beyond that the last-CTA combine spreads over
+    // enough CTAs and the extra launch costs more than it saves (8B B=4: 0.3 us)
+    if (p.max_splits > 1 && (long)batch * hkv <= 16 && ctas <= (long)g_num_sms * g_attn_occupancy) return 4;
+  }
   return cluster_preferred(batch, hq, hkv, max_seq_len) ? 3 : 1;
 }
 
@@ -661,12 +755,12 @@ int attention_split_plan(int batch, int hq, int hkv, int max_seq_len, int num_sm
 }
 
 int attention_variant_for(int batch, int hq, int hkv, int max_seq_len) {
-  return pick_variant(batch, hq, hkv, max_seq_len);
+  return pick_variant(batch, hq, hkv, max_seq_len, /*standalone*/ true);
 }
 
 int set_attention_variant(int variant) {
   const int prev = k1_variant();
-  if (variant >= 0 && variant <= 3) g_k1_variant = variant;
+  if (variant >= 0 && variant <= 4) g_k1_variant = variant;
   return prev;
 }
 
@@ -695,9 +789,9 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
                                     const int32_t* seq_lens, void* workspace,
                                     size_t workspace_bytes, int batch, int hq, int hkv,
                                     int max_seq_len, float scale, cudaStream_t stream,
-                                    bool kv_ready) {
+                                    bool kv_ready, bool standalone) {
   if (batch <= 0) return cudaSuccess;
-  const int variant = pick_variant(batch, hq, hkv, max_seq_len);
+  const int variant = pick_variant(batch, hq, hkv, max_seq_len, standalone);
   if (variant == 3)
     return launch_decode_attention_cluster(map, q, out, block_tables, max_blocks, seq_lens,
                                            workspace, workspace_bytes, batch, hq, hkv,
@@ -737,6 +831,7 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
   a.max_splits = ws_splits;
   a.scale_log2 = scale * 1.4426950408889634f;
   a.kv_ready = kv_ready ? 1 : 0;
+  a.defer_combine = (variant == 4 && plan.max_splits > 1) ? 1 : 0;
   a.trace = k1_trace_buffer();
   a.trace_ctas = a.trace ? k1_trace_capacity() : 0;
   dim3 grid(plan.max_splits, hkv, batch);
@@ -754,8 +849,14 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  if (wide) return cudaLaunchKernelEx(&cfg, paged_gqa_decode_wide_kernel, map, a);
-  return cudaLaunchKernelEx(&cfg, paged_gqa_decode_kernel, map, a);
+  e = wide ? cudaLaunchKernelEx(&cfg, paged_gqa_decode_wide_kernel, map, a)
+           : cudaLaunchKernelEx(&cfg, paged_gqa_decode_kernel, map, a);
+  if (e != cudaSuccess || !a.defer_combine) return e;
+  cudaLaunchConfig_t cc = cfg;
+  cc.gridDim = dim3(a.group, hkv, batch);
+  cc.blockDim = dim3(128);
+  cc.dynamicSmemBytes = 0;
+  return cudaLaunchKernelEx(&cc, attn_combine_kernel, a);
 }
 
 int attention_occupancy() {

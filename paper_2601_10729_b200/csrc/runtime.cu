@@ -27,7 +27,7 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
                                     const int32_t* seq_lens, void* workspace,
                                     size_t workspace_bytes, int batch, int hq, int hkv,
                                     int max_seq_len, float scale, cudaStream_t stream,
-                                    bool kv_ready = false);
+                                    bool kv_ready = false, bool standalone = false);
 cudaError_t launch_kv_append(const void* k_new, const void* v_new, void* pool,
                              const int32_t* block_tables, int max_blocks,
                              const int32_t* positions, const uint64_t* host_slabs,
@@ -345,8 +345,8 @@ const char* ofb_version(void) { return "orbitflow-b200 0.1 sm_100a"; }
 const char* ofb_last_error(void) { return g_err.c_str(); }
 
 int ofb_set_attention_kernel(int32_t variant) {
-  if (variant < 0 || variant > 3)
-    return fail(-1, "variant must be 0 (stream-K), 1 (split), 2 (auto) or 3 (cluster)");
+  if (variant < 0 || variant > 4)
+    return fail(-1, "variant must be 0 (stream-K), 1 (split), 2 (auto), 3 (cluster) or 4 (split2)");
   return ofb::set_attention_variant(variant);
 }
 
@@ -455,7 +455,7 @@ int ofb_decode_attention(const void* q, void* out, const void* kv_pool, int64_t 
   cudaError_t e = ofb::launch_decode_attention(
       map, q, out, block_tables, max_blocks, seq_lens, workspace,
       static_cast<size_t>(workspace_bytes), batch, num_q_heads, num_kv_heads, max_seq_len, scale,
-      static_cast<cudaStream_t>(stream));
+      static_cast<cudaStream_t>(stream), /*kv_ready*/ false, /*standalone*/ true);
   if (e != cudaSuccess) return cuda_fail(e, "paged_gqa_decode_kernel launch");
   return 0;
 }

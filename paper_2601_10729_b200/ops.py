@@ -125,9 +125,10 @@ def device_info() -> tuple[int, int]:
 
 def set_attention_kernel(variant: str) -> str:
     """Select K1's work decomposition: "stream" (persistent stream-K), "split"
-    (fixed splits + last-CTA combine), "cluster" (cluster splits, DSMEM combine)
+    (fixed splits + last-CTA combine), "cluster" (cluster splits, DSMEM combine),
+    "split2" (fixed splits + a second, programmatically launched combine kernel)
     or "auto" (default).  Returns the previous one."""
-    names = {"stream": 0, "split": 1, "auto": 2, "cluster": 3}
+    names = {"stream": 0, "split": 1, "auto": 2, "cluster": 3, "split2": 4}
     prev = _native.load().ofb_set_attention_kernel(names[variant])
     if prev < 0:
         _native.check(prev, "ofb_set_attention_kernel")

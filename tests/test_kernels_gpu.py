@@ -17,9 +17,11 @@ pytestmark = pytest.mark.gpu
 RTOL, ATOL = 2e-2, 1e-2
 
 
-@pytest.fixture(params=["stream", "split", "cluster"], autouse=True)
+@pytest.fixture(params=["stream", "split", "split2", "cluster", "auto"], autouse=True)
 def k1_variant(request):
-    """Every K1 parity test runs under both work decompositions."""
+    """Every K1 parity test runs under every work decomposition (stream-K, split
+    with the in-kernel combine, split with the separate combine kernel, cluster)
+    and under the auto policy."""
     from paper_2601_10729_b200 import ops
 
     prev = ops.set_attention_kernel(request.param)

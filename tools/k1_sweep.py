@@ -60,7 +60,7 @@ for hq, hkv, label in [(32, 8, "8B (32q/8kv)"), (8, 1, "70B TP8 shard (8q/1kv)")
                 times.append(e0.elapsed_time(e1) / iters)
             us = statistics.median(times) * 1e3
             alg = batch * seq * hkv * 512 + 2 * batch * hq * 128 * 2
-            variant = {0: "stream-K", 1: "split", 3: "cluster"}.get(int(lib.ofb_attention_variant_for(batch, hkv, seq)), "?")
+            variant = {0: "stream-K", 1: "split", 3: "cluster", 4: "split2"}.get(int(lib.ofb_attention_variant_for(batch, hkv, seq)), "?")
             row = {"heads": label, "batch": batch, "seq": seq, "us": us, "GBps": alg / us / 1e3,
                    "frac_of_copy_peak": alg / us / 1e3 / PEAK, "variant": variant}
             rows.append(row)

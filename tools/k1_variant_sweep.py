@@ -1,6 +1,6 @@
 """K1 work decompositions side by side on latency-bound and transitional shapes:
-split (global last-CTA combine) vs cluster (DSMEM combine) at cluster caps
-16 / 8 / 4.  Graph-replayed back-to-back launches (device time per launch), and
+split (global last-CTA combine), split2 (a separate combine kernel) and cluster
+(DSMEM combine) at cluster caps 16 / 8 / 4.  Graph-replayed back-to-back launches (device time per launch), and
 each variant's output compared with the split kernel's (max |diff|).  One JSON
 line per point on stderr, a markdown table on stdout.
 
@@ -26,7 +26,7 @@ except Exception:
 dev = torch.device("cuda:0")
 lib = _native.load()
 quick = "--quick" in sys.argv
-VARIANTS = [("split", None), ("cluster16", "16"), ("cluster8", "8"), ("cluster4", "4")]
+VARIANTS = [("split", None), ("split2", None), ("cluster16", "16"), ("cluster8", "8"), ("cluster4", "4")]
 shapes = []
 for hq, hkv, label in [(32, 8, "8B"), (8, 1, "70B-TP8"), (64, 8, "70B")]:
     for batch in ((1, 4) if quick else (1, 2, 4, 8, 16)):
@@ -78,7 +78,7 @@ for hq, hkv, label, batch, seq in shapes:
     for name, cap in VARIANTS:
         if cap is None:
             os.environ.pop("OFB_K1_CLUSTER", None)
-            ops.set_attention_kernel("split")
+            ops.set_attention_kernel(name)
         else:
             os.environ["OFB_K1_CLUSTER"] = cap
             ops.set_attention_kernel("cluster")
@@ -97,14 +97,14 @@ for hq, hkv, label, batch, seq in shapes:
             diff = float((out.float() - ref).abs().max())
         row[name] = round(us, 2)
         row[name + "_maxdiff"] = diff
-    for name, cap in VARIANTS[1:]:
+    for name, cap in VARIANTS[2:]:
         os.environ["OFB_K1_CLUSTER"] = cap
         plan = ops.cluster_plan(batch, hkv, seq)
         row[name + "_plan"] = None if plan is None else (plan["cluster"], plan["clusters_per_pair"],
                                                           plan["blocks_per_cta"])
     os.environ.pop("OFB_K1_CLUSTER", None)
     ops.set_attention_kernel("auto")
-    row["auto_pick"] = {0: "stream", 1: "split", 3: "cluster"}.get(
+    row["auto_pick"] = {0: "stream", 1: "split", 3: "cluster", 4: "split2"}.get(
         int(lib.ofb_attention_variant_for(batch, hkv, seq)), "?")
     row["alg_bytes"] = alg
     rows.append(row)
