@@ -170,7 +170,10 @@ typedef struct ofb_step_desc {
   /* 0: one append of every resident row at step start (the token's K/V of all
    * layers is known up front).  1: the append of layer l runs right before its
    * attention, inside ofb_runtime_step_layers - a decoder whose k_new/v_new of
-   * layer l are produced by work the caller interleaves after layer l-1. */
+   * layer l are produced by work the caller interleaves after layer l-1.  2: as
+   * 1, but the producer of k_new/v_new already wrote the resident rows into the
+   * pool (ofb_oproj_desc.kv_pool): only rows with a host slab are appended
+   * (host slab + staging), and a layer without fetches launches no append. */
   int32_t append_per_layer;
 } ofb_step_desc;
 
@@ -323,6 +326,19 @@ typedef struct ofb_oproj_desc {
   /* x_layers: 0 = x holds `layers` layers and layer `layer` is read; 1 = x is one
    * bf16 [batch][k] input for every layer (the decoder's residual stream). */
   int32_t x_layers;
+  /* K3 folded into a q/k/v projection (world 1, out_parts): parts kv_part and
+   * kv_part + 1 are k and v of part_cols/128 local KV heads; each batch row's
+   * token is also written to the paged pool at slot kv_positions[b] of block
+   * kv_tables[b][pos/16] (bytes kv_block_bytes per block, layout of
+   * ofb_kv_append), for rows whose kv_host_slabs[b] is 0 (NULL: all rows);
+   * rows with a host slab are left to the runtime's append. NULL kv_pool = off. */
+  void* kv_pool;
+  const int32_t* kv_tables;     /* [batch][kv_max_blocks] of this layer */
+  const int32_t* kv_positions;  /* [batch], < 0 = skip */
+  const uint64_t* kv_host_slabs;
+  int32_t kv_max_blocks;
+  int32_t kv_part;
+  int64_t kv_block_bytes;
 } ofb_oproj_desc;
 
 OFB_API int ofb_oproj_allreduce(const ofb_oproj_desc* desc, void* stream);

@@ -94,6 +94,8 @@ class OprojDesc(ctypes.Structure):
         ("out_parts", c_i32), ("part_cols", c_i32 * 4), ("part_out", c_vp * 4),
         ("ss_out", c_vp), ("ss_in", c_vp), ("ss_tiles", c_i32), ("eps", ctypes.c_float),
         ("swiglu", c_i32), ("x_layers", c_i32),
+        ("kv_pool", c_vp), ("kv_tables", c_vp), ("kv_positions", c_vp), ("kv_host_slabs", c_vp),
+        ("kv_max_blocks", c_i32), ("kv_part", c_i32), ("kv_block_bytes", c_i64),
     ]
 
 

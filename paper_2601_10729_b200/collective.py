@@ -204,7 +204,7 @@ class OprojAllReduce:
                  stream=None, residual: torch.Tensor | None = None,
                  parts: list | None = None, ss_out: torch.Tensor | None = None,
                  ss_in: torch.Tensor | None = None, eps: float = 1e-5,
-                 swiglu: bool = False) -> torch.Tensor:
+                 swiglu: bool = False, kv_append: dict | None = None) -> torch.Tensor:
         """``x``: bf16 [L, B, K] (or [L, B, Hq_local, 128]) - all layers' attention
         output; layer ``layer`` is projected.  A 2-D ``x`` [B, K] is one input for
         every layer (the decoder's residual stream).  Returns bf16 [B, H].
@@ -216,7 +216,12 @@ class OprojAllReduce:
         ``ss_in`` (such a tensor from the launch that produced ``x``) scales output
         row b by rsqrt(mean(x[b]^2) + eps), so the projection consumes
         RMSNorm(x) with the norm weight folded into W.  ``swiglu``: W was packed
-        with ``interleave_gate_up`` and ``out`` is bf16 [B, H/2] = silu(gate) * up."""
+        with ``interleave_gate_up`` and ``out`` is bf16 [B, H/2] = silu(gate) * up.
+        ``kv_append`` (with ``parts`` = q, k, v): K3 folded in - the k / v rows are
+        also written to the token's slot of the paged pool; keys ``pool``,
+        ``tables`` (this layer's [B, max_blocks] int32 device pointer),
+        ``positions``, ``host_slabs`` (device pointer or 0), ``max_blocks``,
+        ``part`` (index of the k part) and ``block_bytes``."""
         if not x.is_cuda or x.dtype != torch.bfloat16:
             raise ValueError("x must be a bf16 CUDA tensor (no CPU fallback)")
         if x.dim() == 2:             # one input for every layer (W of `layer`)
@@ -272,6 +277,13 @@ class OprojAllReduce:
             d.ss_in, d.ss_tiles = ss_in.data_ptr(), ss_in.shape[0]
         d.eps = float(eps)
         d.swiglu = 1 if swiglu else 0
+        if kv_append is not None:
+            if parts is None:
+                raise ValueError("kv_append needs the q / k / v parts")
+            d.kv_pool, d.kv_tables = kv_append["pool"], kv_append["tables"]
+            d.kv_positions, d.kv_host_slabs = kv_append["positions"], kv_append.get("host_slabs") or None
+            d.kv_max_blocks, d.kv_part = kv_append["max_blocks"], kv_append["part"]
+            d.kv_block_bytes = kv_append["block_bytes"]
         d.workspace, d.workspace_bytes = self.ws.data_ptr(), self.ws.numel()
         d.max_batch = self.max_batch
         d.status = self._status.data_ptr()

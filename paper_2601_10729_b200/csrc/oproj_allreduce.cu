@@ -70,6 +70,12 @@ struct OprojArgs {
   float eps;
   int swiglu;                      // 1: rows interleaved gate 64 / up 64; out [batch][hidden/2] = silu(g) * u
   int x_layer;                     // x's layer coordinate (0 when one x serves every layer)
+  uint8_t* kv_pool;                // K3 folded in (see ofb_oproj_desc), or null
+  const int32_t* kv_tables;
+  const int32_t* kv_positions;
+  const uint64_t* kv_host;
+  int kv_max_blocks, kv_part;
+  long long kv_block_bytes;
   int part_lo[5];                  // first column of range i (part_lo[parts] = hidden)
   __nv_bfloat16* part_out[4];
 };
@@ -298,6 +304,32 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
   // MMAs still run.  out[b] = (x[b] . W'^T) * rsqrt(mean(x[b]^2) + eps), the
   // norm weight having been folded into W' (pack time).
   __shared__ float rsc[256];
+  __shared__ long long kvoff[256];   // K3 folded in: pool byte offset of each row's slot, or -1
+  // the k / v part this tile belongs to (one KV head's 128 dims), if K3 is folded in
+  int kvsel = -1;
+  if (a.kv_pool) {
+    for (int r = 0; r < a.parts; ++r)
+      if (tile * kTileM >= a.part_lo[r] && tile * kTileM < a.part_lo[r + 1]) kvsel = r - a.kv_part;
+    if (kvsel != 0 && kvsel != 1) kvsel = -1;
+  }
+  if (kvsel >= 0 && split == 0) {
+    // resolve every row's slot while the MMAs run (two dependent loads per row
+    // would otherwise sit on the epilogue's critical path)
+    pdl_wait();
+    const int head = (tile * kTileM - a.part_lo[a.kv_part + kvsel]) / kTileM;
+    for (int b = threadIdx.x; b < a.batch; b += kThreads) {
+      long long off = -1;
+      const int pos = a.kv_positions[b];
+      if (pos >= 0 && (!a.kv_host || a.kv_host[b] == 0)) {
+        const int blk = a.kv_tables[static_cast<size_t>(b) * a.kv_max_blocks + pos / kBlockTokens];
+        if (blk >= 0)
+          off = static_cast<long long>(blk) * a.kv_block_bytes +
+                static_cast<long long>((head * 2 + kvsel) * kBlockTokens + pos % kBlockTokens) * kRowBytes;
+      }
+      kvoff[b] = off;
+    }
+    if (a.splits == 1 && !a.ss_in) __syncthreads();   // else a barrier below publishes kvoff
+  }
   if (a.ss_in && split == 0) {
     pdl_wait();
     for (int b = threadIdx.x; b < a.batch; b += kThreads) {
@@ -422,16 +454,23 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
   if (a.world == 1) {
     // the column range (tensor) this tile belongs to: one lookup per CTA
     __nv_bfloat16* dst_base = a.out;
-    int dst_stride = a.hidden, col0 = tile * kTileM;
+    int dst_stride = a.hidden, col0 = tile * kTileM, part = -1;
     for (int r = 0; r < a.parts; ++r)
       if (col0 >= a.part_lo[r] && col0 < a.part_lo[r + 1]) {
         dst_base = a.part_out[r];
         dst_stride = a.part_lo[r + 1] - a.part_lo[r];
         col0 -= a.part_lo[r];
+        part = r;
       }
+    // K3 folded in: a k or v tile is one KV head's 128 dims; its rows also go to
+    // the token's slot in the paged pool (resident rows; host-slab rows are the
+    // runtime append's, which also fills their staged copy)
+    (void)part;
     for (int i = threadIdx.x; i < nvec; i += kThreads) {
       const int b = i >> 4, o = i & 15;
       *reinterpret_cast<uint4*>(dst_base + static_cast<size_t>(b) * dst_stride + col0 + o * 8) = s4[i];
+      if (kvsel >= 0 && kvoff[b] >= 0)
+        *reinterpret_cast<uint4*>(a.kv_pool + kvoff[b] + o * 16) = s4[i];
     }
     if (tr) tr[5] = globaltimer();
     return;
@@ -794,6 +833,18 @@ int ofb_oproj_allreduce(const ofb_oproj_desc* d, void* stream) {
   a.swiglu = d->swiglu;
   if (d->x_layers != 0 && d->x_layers != 1) return report_error(-1, "ofb_oproj_allreduce: x_layers must be 0 or 1");
   a.x_layer = d->x_layers == 1 ? 0 : d->layer;
+  a.kv_pool = static_cast<uint8_t*>(d->kv_pool);
+  a.kv_tables = d->kv_tables;
+  a.kv_positions = d->kv_positions;
+  a.kv_host = d->kv_host_slabs;
+  a.kv_max_blocks = d->kv_max_blocks;
+  a.kv_part = d->kv_part;
+  a.kv_block_bytes = d->kv_block_bytes;
+  if (d->kv_pool && (d->world != 1 || a.parts < 2 || d->kv_part < 0 || d->kv_part + 1 >= a.parts ||
+                     !d->kv_tables || !d->kv_positions || d->kv_max_blocks < 1 || d->kv_block_bytes <= 0 ||
+                     d->part_cols[d->kv_part] != d->part_cols[d->kv_part + 1]))
+    return report_error(-1, "ofb_oproj_allreduce: kv_pool needs world 1, k / v parts of equal width, "
+                            "tables, positions and a block size");
   if (d->ss_in && (d->world != 1 || d->ss_tiles < 1 || !(d->eps >= 0.f)))
     return report_error(-1, "ofb_oproj_allreduce: ss_in needs world 1, ss_tiles >= 1 and eps >= 0");
   if (d->swiglu && (d->world != 1 || d->residual || a.parts || d->ss_out || !d->out))

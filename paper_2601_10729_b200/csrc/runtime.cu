@@ -715,13 +715,13 @@ int step_layers(ofb_runtime* rt, int count) {
         layer_fetches = true;
       }
     }
-    if (layer_fetches || d->append_per_layer) {
+    if (layer_fetches || d->append_per_layer == 1) {
       const size_t kv_layer = (size_t)B * d->num_kv_heads * ofb::kHeadDim * 2;
       e = ofb::launch_kv_append(static_cast<const uint8_t*>(d->k_new) + l * kv_layer,
                                 static_cast<const uint8_t*>(d->v_new) + l * kv_layer, d->kv_pool,
                                 d->block_tables + l * bt_layer, d->max_blocks, d->positions,
                                 d->host_slabs_dev + (size_t)l * B, 1, B, d->num_kv_heads,
-                                d->append_per_layer ? /*kAppendAll*/ 1 : /*kAppendOffloaded*/ 2, cs,
+                                d->append_per_layer == 1 ? /*kAppendAll*/ 1 : /*kAppendOffloaded*/ 2, cs,
                                 /*pdl*/ d->append_per_layer && !layer_fetches);
       if (e != cudaSuccess) return cuda_fail(e, "kv_append_kernel launch");
     }

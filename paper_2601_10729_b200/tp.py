@@ -362,7 +362,10 @@ class TensorParallelLlama:
         bufs = self._buffers(B)
         q, kn, vn = bufs["q"], bufs["k_new"], bufs["v_new"]
         desc, keep = ex.prepare_step(batch, {"q": q, "k_new": kn, "v_new": vn})
-        desc.append_per_layer = 1
+        k6 = self.c1 == "k6"
+        # K6 writes the resident rows' new K/V straight into the pool (K3 folded
+        # into the q/k/v epilogue); the runtime appends only host-slab rows
+        desc.append_per_layer = 2 if k6 else 1
         out = keep[1]
         stream = torch.cuda.current_stream()
         x = bufs["x"][ex.steps % 2]
@@ -370,8 +373,10 @@ class TensorParallelLlama:
         h = bufs["h"]
         nq, nk = self.shard.local_q * 128, self.shard.local_kv * 128
         a_all, a2_all, gu = bufs["a"], bufs["a2"], bufs["gu"]
-        k6 = self.c1 == "k6"
         ss = bufs["ss"]
+        kv_base = {"pool": desc.kv_pool, "positions": desc.positions, "max_blocks": desc.max_blocks,
+                   "part": 1, "block_bytes": ex.shape.block_bytes}
+        bt_layer = B * desc.max_blocks * 4
         if k6:   # the first layer's fused RMSNorm: row sums of squares of the embeddings
             from . import _native
 
@@ -381,8 +386,11 @@ class TensorParallelLlama:
         try:
             for l in range(L):
                 a = a_all[l]
-                if k6:     # RMSNorm(x) . W_qkv^T for this rank's heads in one launch, into their buffers
-                    self.qkv_proj(x, l, stream=stream, ss_in=ss, eps=self.eps,
+                if k6:     # RMSNorm(x) . W_qkv^T for this rank's heads in one launch, into their
+                    # buffers, the new token's K/V also into its pool slot (resident rows)
+                    kv = dict(kv_base, tables=desc.block_tables + l * bt_layer,
+                              host_slabs=desc.host_slabs_dev + l * B * 8)
+                    self.qkv_proj(x, l, stream=stream, ss_in=ss, eps=self.eps, kv_append=kv,
                                   parts=[q[l].view(B, nq), kn[l].view(B, nk), vn[l].view(B, nk)])
                 else:
                     self._rmsnorm(x, self.norm[0], a, stream)
