@@ -52,7 +52,9 @@ struct AttnArgs {
   int hq, hkv, group;
   int blocks_per_split, max_splits;
   float scale_log2;
-  int kv_ready;                 // 1: KV complete before the PDL wait (see the stream kernel)
+  int kv_ready;                 // 1: KV complete before the PDL wait (see the stream kernel);
+                                // 2: all but each request's last block (the one receiving
+                                //    this step's token, written by the predecessor)
   int defer_combine;            // 1: multi-split pairs stop after their partials (attn_combine_kernel)
   unsigned long long* trace;    // diagnostics (ofb_k1_trace): kSplitTraceSlots stamps per CTA
   int trace_ctas;               // capacity of `trace` in CTAs
@@ -196,9 +198,11 @@ __device__ __forceinline__ void paged_gqa_decode_body(const CUtensorMap& kv_map,
   if (warp == kW) {
     // ---------------------------------------------------------- producer
     if (lane == 0) {
+      const int last_blk = (seq - 1) / kBlockTokens;   // block of this step's token
       for (int i = 0; i < n; ++i) {
         const int st = i % kS;
         if (i >= kS) mbar_wait(&empty[st], ((i / kS) - 1) & 1);
+        if (a.kv_ready == 2 && b_begin + i == last_blk) pdl_wait();   // the token's K/V is the predecessor's
         const int row = (blk_ids[i] * a.hkv + kvh) * kTileRows;
         uint8_t* dst = ring + (size_t)st * kHeadBlockBytes;
         mbar_arrive_expect_tx(&full[st], kHeadBlockBytes);
@@ -789,17 +793,17 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
                                     const int32_t* seq_lens, void* workspace,
                                     size_t workspace_bytes, int batch, int hq, int hkv,
                                     int max_seq_len, float scale, cudaStream_t stream,
-                                    bool kv_ready, bool standalone) {
+                                    int kv_ready, bool standalone) {
   if (batch <= 0) return cudaSuccess;
   const int variant = pick_variant(batch, hq, hkv, max_seq_len, standalone);
   if (variant == 3)
     return launch_decode_attention_cluster(map, q, out, block_tables, max_blocks, seq_lens,
                                            workspace, workspace_bytes, batch, hq, hkv,
-                                           max_seq_len, scale, stream, kv_ready);
+                                           max_seq_len, scale, stream, kv_ready == 1);
   if (variant == 0)
     return launch_decode_attention_stream(map, q, out, block_tables, max_blocks, seq_lens,
                                           workspace, workspace_bytes, batch, hq, hkv, max_seq_len,
-                                          scale, stream, kv_ready);
+                                          scale, stream, kv_ready == 1);
   if (hkv <= 0 || hq % hkv != 0 || hq / hkv > kMaxGroup) return cudaErrorInvalidValue;
   if ((size_t)batch * hkv * sizeof(int32_t) > kCounterRegionBytes) return cudaErrorInvalidValue;
   cudaError_t e = attn_init_once();
@@ -830,7 +834,7 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
   a.blocks_per_split = plan.blocks_per_split;
   a.max_splits = ws_splits;
   a.scale_log2 = scale * 1.4426950408889634f;
-  a.kv_ready = kv_ready ? 1 : 0;
+  a.kv_ready = kv_ready;
   a.defer_combine = (variant == 4 && plan.max_splits > 1) ? 1 : 0;
   a.trace = k1_trace_buffer();
   a.trace_ctas = a.trace ? k1_trace_capacity() : 0;

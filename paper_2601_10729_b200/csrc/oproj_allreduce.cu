@@ -343,7 +343,8 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
   if (tr) tr[2] = globaltimer();
   tc_fence_after();
   pdl_wait();                       // every thread: the predecessor's writes are visible
-  pdl_trigger();                    // the next kernel may start its own prologue
+  pdl_trigger();                    // the next kernel may start its own prologue (releasing it
+                                    // right after the prologue measured slower in the decoder step)
   const int m = warp * 32 + lane;
   const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
   // leader smem: red [splits-1][npad][128] fp32 after the ring (its own region, so
@@ -840,6 +841,7 @@ int ofb_oproj_allreduce(const ofb_oproj_desc* d, void* stream) {
   a.kv_max_blocks = d->kv_max_blocks;
   a.kv_part = d->kv_part;
   a.kv_block_bytes = d->kv_block_bytes;
+
   if (d->kv_pool && (d->world != 1 || a.parts < 2 || d->kv_part < 0 || d->kv_part + 1 >= a.parts ||
                      !d->kv_tables || !d->kv_positions || d->kv_max_blocks < 1 || d->kv_block_bytes <= 0 ||
                      d->part_cols[d->kv_part] != d->part_cols[d->kv_part + 1]))

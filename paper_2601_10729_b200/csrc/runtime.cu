@@ -27,7 +27,7 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
                                     const int32_t* seq_lens, void* workspace,
                                     size_t workspace_bytes, int batch, int hq, int hkv,
                                     int max_seq_len, float scale, cudaStream_t stream,
-                                    bool kv_ready = false, bool standalone = false);
+                                    int kv_ready = 0, bool standalone = false);
 cudaError_t launch_kv_append(const void* k_new, const void* v_new, void* pool,
                              const int32_t* block_tables, int max_blocks,
                              const int32_t* positions, const uint64_t* host_slabs,
@@ -455,7 +455,7 @@ int ofb_decode_attention(const void* q, void* out, const void* kv_pool, int64_t 
   cudaError_t e = ofb::launch_decode_attention(
       map, q, out, block_tables, max_blocks, seq_lens, workspace,
       static_cast<size_t>(workspace_bytes), batch, num_q_heads, num_kv_heads, max_seq_len, scale,
-      static_cast<cudaStream_t>(stream), /*kv_ready*/ false, /*standalone*/ true);
+      static_cast<cudaStream_t>(stream), /*kv_ready*/ 0, /*standalone*/ true);
   if (e != cudaSuccess) return cuda_fail(e, "paged_gqa_decode_kernel launch");
   return 0;
 }
@@ -733,7 +733,11 @@ int step_layers(ofb_runtime* rt, int count) {
     // KV of a layer with no fetch this step was complete before the previous
     // layer's K1 passed its dependency wait (step-start append), so K1 may stream
     // it before its own wait; q / outputs / workspace still wait.
-    const bool kv_ready = l > 0 && !layer_fetches && !d->append_per_layer;
+    // (2: the whole-decoder step with K3 folded into the q/k/v projection - all of
+    // the layer's KV but the blocks receiving this step's token predates it)
+    const int kv_ready = (l > 0 && !layer_fetches && !d->append_per_layer) ? 1
+                         : (!layer_fetches && d->append_per_layer == 2) ? 2
+                                                                         : 0;
     e = ofb::launch_decode_attention(
         st.map, static_cast<const uint8_t*>(d->q) + l * q_layer,
         static_cast<uint8_t*>(d->out) + l * q_layer, d->block_tables + l * bt_layer, d->max_blocks,
