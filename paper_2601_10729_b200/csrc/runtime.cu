@@ -735,9 +735,10 @@ int step_layers(ofb_runtime* rt, int count) {
     // it before its own wait; q / outputs / workspace still wait.
     // (2: the whole-decoder step with K3 folded into the q/k/v projection - all of
     // the layer's KV but the blocks receiving this step's token predates it)
+    // (the first layer of an ordinary step follows the step-start append: the same)
     const int kv_ready = (l > 0 && !layer_fetches && !d->append_per_layer) ? 1
-                         : (!layer_fetches && d->append_per_layer == 2) ? 2
-                                                                         : 0;
+                         : (!layer_fetches && (d->append_per_layer == 2 || (l == 0 && !d->append_per_layer))) ? 2
+                                                                                                            : 0;
     e = ofb::launch_decode_attention(
         st.map, static_cast<const uint8_t*>(d->q) + l * q_layer,
         static_cast<uint8_t*>(d->out) + l * q_layer, d->block_tables + l * bt_layer, d->max_blocks,
