@@ -14,7 +14,7 @@ from paper_2601_10729_b200.core import PlacementMatrix, RequestState  # noqa: E4
 from paper_2601_10729_b200.executor import B200Executor, ModelShape  # noqa: E402
 
 dev = torch.device("cuda:0")
-for variant in ("stream", "split"):
+for variant in ("stream", "split", "split2", "cluster"):
     ops.set_attention_kernel(variant)
     for lens in ([700, 33, 1, 0, 255], [3000]):
         case = make_case(lens, 8, 2, seed=1)
@@ -75,5 +75,30 @@ for bsz, k, h in [(5, 128, 1024), (32, 1024, 2048)]:
     w = (torch.randn((2, h, k), device=dev) * k ** -0.5).to(torch.bfloat16)
     x = torch.randn((2, bsz, k), device=dev).to(torch.bfloat16)
     OprojAllReduce(w, bsz)(x, 1)
+# K6 decoder-layer epilogues: fused RMSNorm (ss_out -> ss_in), SwiGLU, K3 fold
+from paper_2601_10729_b200.collective import interleave_gate_up  # noqa: E402
+
+bsz, k, h = 7, 256, 512
+w = (torch.randn((2, h, k), device=dev) * k ** -0.5).to(torch.bfloat16)
+x = torch.randn((bsz, h), device=dev).to(torch.bfloat16)
+ss = torch.zeros((h // 128, 8), dtype=torch.float32, device=dev)
+OprojAllReduce(w, 8)(torch.randn((2, bsz, k), device=dev).to(torch.bfloat16), 0, out=x, residual=x, ss_out=ss)
+wgu = interleave_gate_up((torch.randn((2, 2 * 256, h), device=dev) * h ** -0.5).to(torch.bfloat16))
+OprojAllReduce(wgu, 8)(x, 1, ss_in=ss, swiglu=True)
+from paper_2601_10729_b200.tp import HeadShard, TensorParallelLlama  # noqa: E402
+
+shape = ModelShape(2, 8, 2)
+ex = B200Executor(shape, device_blocks=600, host_blocks=600, staging_slots=2)
+dec = TensorParallelLlama(ex, HeadShard(0, 1, 8, 2), 256, 512, c1="k6", max_batch=3)
+batch = [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=150 + 61 * i, target_output_tokens=8)
+         for i in range(3)]
+pm = PlacementMatrix(tuple(r.id for r in batch), 2, ((1, 0), (1, 1), (0, 1)))
+ex.install(batch, pm)
+for _ in range(2):
+    dec.step(batch, torch.randn((3, 256), device=dev).to(torch.bfloat16))
+    for r in batch:
+        r.record_generated_token()
 torch.cuda.synchronize()
+dec.close()
+ex.close()
 print("sanitize case done")
