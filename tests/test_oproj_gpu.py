@@ -145,7 +145,7 @@ def test_cluster_split_counts_agree_with_fp32(monkeypatch, splits):
     from paper_2601_10729_b200.collective import OprojAllReduce
 
     dev = torch.device("cuda:0")
-    b, k, h = 19, 1280, 1280
+    b, k, h = 19, 4096, 1280          # 64 K chunks: >= 4 per CTA even at 8 splits
     xs, ws = _inputs(1, 2, b, k, h, seed=40 + splits)
     monkeypatch.setenv("OFB_K6_SPLITS", str(splits))
     op = OprojAllReduce(ws[0].to(dev), max_batch=32)
