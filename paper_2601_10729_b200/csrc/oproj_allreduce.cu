@@ -786,6 +786,21 @@ int ofb_oproj_allreduce(const ofb_oproj_desc* d, void* stream) {
     for (int r = 0; r < d->world; ++r)
       if (!d->symm[r]) return report_error(-1, "ofb_oproj_allreduce: missing peer buffer");
   }
+  {  // the decoder-layer epilogues (validated before any driver call)
+    const int parts = d->out_parts > 1 ? d->out_parts : 0;
+    if (d->ss_in && (d->world != 1 || d->ss_tiles < 1 || !(d->eps >= 0.f)))
+      return report_error(-1, "ofb_oproj_allreduce: ss_in needs world 1, ss_tiles >= 1 and eps >= 0");
+    if (d->swiglu && (d->world != 1 || d->residual || parts || d->ss_out || !d->out))
+      return report_error(-1, "ofb_oproj_allreduce: swiglu needs world 1, an out tensor, no residual / parts / ss_out");
+    if (d->ss_out && parts) return report_error(-1, "ofb_oproj_allreduce: ss_out excludes out_parts");
+    if (d->x_layers != 0 && d->x_layers != 1)
+      return report_error(-1, "ofb_oproj_allreduce: x_layers must be 0 or 1");
+    if (d->kv_pool && (d->world != 1 || parts < 2 || d->kv_part < 0 || d->kv_part + 1 >= parts ||
+                       !d->kv_tables || !d->kv_positions || d->kv_max_blocks < 1 || d->kv_block_bytes <= 0 ||
+                       d->part_cols[d->kv_part] != d->part_cols[d->kv_part + 1]))
+      return report_error(-1, "ofb_oproj_allreduce: kv_pool needs world 1, k / v parts of equal width, "
+                              "tables, positions and a block size");
+  }
   const int npad = padded_batch(d->batch);
   const int tiles = d->hidden / kTileM;
   const int chunks = d->k / kChunkK;
@@ -836,7 +851,6 @@ int ofb_oproj_allreduce(const ofb_oproj_desc* d, void* stream) {
   a.ss_tiles = d->ss_tiles;
   a.eps = d->eps;
   a.swiglu = d->swiglu;
-  if (d->x_layers != 0 && d->x_layers != 1) return report_error(-1, "ofb_oproj_allreduce: x_layers must be 0 or 1");
   a.x_layer = d->x_layers == 1 ? 0 : d->layer;
   a.kv_pool = static_cast<uint8_t*>(d->kv_pool);
   a.kv_tables = d->kv_tables;
@@ -846,16 +860,8 @@ int ofb_oproj_allreduce(const ofb_oproj_desc* d, void* stream) {
   a.kv_part = d->kv_part;
   a.kv_block_bytes = d->kv_block_bytes;
 
-  if (d->kv_pool && (d->world != 1 || a.parts < 2 || d->kv_part < 0 || d->kv_part + 1 >= a.parts ||
-                     !d->kv_tables || !d->kv_positions || d->kv_max_blocks < 1 || d->kv_block_bytes <= 0 ||
-                     d->part_cols[d->kv_part] != d->part_cols[d->kv_part + 1]))
-    return report_error(-1, "ofb_oproj_allreduce: kv_pool needs world 1, k / v parts of equal width, "
-                            "tables, positions and a block size");
-  if (d->ss_in && (d->world != 1 || d->ss_tiles < 1 || !(d->eps >= 0.f)))
-    return report_error(-1, "ofb_oproj_allreduce: ss_in needs world 1, ss_tiles >= 1 and eps >= 0");
-  if (d->swiglu && (d->world != 1 || d->residual || a.parts || d->ss_out || !d->out))
-    return report_error(-1, "ofb_oproj_allreduce: swiglu needs world 1, an out tensor, no residual / parts / ss_out");
-  if (d->ss_out && a.parts) return report_error(-1, "ofb_oproj_allreduce: ss_out excludes out_parts");
+
+
 
   const size_t smem = static_cast<size_t>(a.stages) * stage_bytes + red_bytes(splits, npad) + 1024;
   {  // the dynamic-smem opt-in is per device: set it once for each device used

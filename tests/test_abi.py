@@ -91,9 +91,28 @@ def test_k6_host_sizing_and_argument_errors():
     for bad, msg in [(dict(batch=9), "max_batch"), (dict(k=96), "multiple of 64"),
                      (dict(hidden=200), "multiple of 128"), (dict(layer=2), "layer"),
                      (dict(world=2, rank=0, epoch=0), "epoch"), (dict(w_layout=3), "w_layout"),
-                     (dict(world=9), "world")]:
+                     (dict(world=9), "world"),
+                     # decoder-layer epilogues
+                     (dict(ss_in=1 << 20, ss_tiles=0), "ss_in"), (dict(ss_in=1 << 20, ss_tiles=2, eps=-1.0), "ss_in"),
+                     (dict(swiglu=1, residual=1 << 20), "swiglu"),
+                     (dict(out_parts=2, ss_out=1 << 20), "ss_out excludes"),
+                     (dict(x_layers=2), "x_layers"),
+                     (dict(kv_pool=1 << 20), "kv_pool")]:
         rc, err = call(**bad)
         assert rc == -1 and msg in err, (bad, rc, err)
+
+
+def test_gate_up_interleave_round_trip():
+    """The SwiGLU epilogue's weight order: rows interleaved per 64 (gate, up) and back."""
+    import torch
+
+    from paper_2601_10729_b200.collective import deinterleave_gate_up, interleave_gate_up
+
+    w = torch.arange(2 * 2 * 192 * 3, dtype=torch.float32).reshape(2, 2 * 192, 3)
+    v = interleave_gate_up(w)
+    assert torch.equal(v[:, 64:128], w[:, 192:256])          # tile 0: gate 0..63 then up 0..63
+    assert torch.equal(v[:, 128:192], w[:, 64:128])
+    assert torch.equal(deinterleave_gate_up(v), w)
 
 
 def test_runtime_calls_without_a_runtime_fail_cleanly():
