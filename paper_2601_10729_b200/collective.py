@@ -205,7 +205,27 @@ class OprojAllReduce:
                  parts: list | None = None, ss_out: torch.Tensor | None = None,
                  ss_in: torch.Tensor | None = None, eps: float = 1e-5,
                  swiglu: bool = False, kv_append: dict | None = None) -> torch.Tensor:
-        """``x``: bf16 [L, B, K] (or [L, B, Hq_local, 128]) - all layers' attention
+        """Validate, build the descriptor and launch (``prepare`` + ``launch``)."""
+        d, result = self.prepare(x, layer, out=out, residual=residual, parts=parts, ss_out=ss_out,
+                                 ss_in=ss_in, eps=eps, swiglu=swiglu, kv_append=kv_append)
+        s = stream if stream is not None else torch.cuda.current_stream(x.device)
+        self.launch(d, s.cuda_stream)
+        return result
+
+    def launch(self, d, stream_handle: int) -> None:
+        """Launch a descriptor from ``prepare`` (reusable across calls: its tensors
+        must stay alive; an exchange takes the next epoch here)."""
+        if d.world > 1:
+            d.epoch = self.symm.next_epoch()
+        _check(_lib().ofb_oproj_allreduce(ctypes.byref(d), ctypes.c_void_p(stream_handle)),
+               "ofb_oproj_allreduce")
+
+    def prepare(self, x: torch.Tensor, layer: int, out: torch.Tensor | None = None,
+                residual: torch.Tensor | None = None, parts: list | None = None,
+                ss_out: torch.Tensor | None = None, ss_in: torch.Tensor | None = None,
+                eps: float = 1e-5, swiglu: bool = False, kv_append: dict | None = None):
+        """Validate the arguments and build the ``ofb_oproj_desc`` (no launch);
+        returns ``(desc, out or parts)``.  ``x``: bf16 [L, B, K] (or [L, B, Hq_local, 128]) - all layers' attention
         output; layer ``layer`` is projected.  A 2-D ``x`` [B, K] is one input for
         every layer (the decoder's residual stream).  Returns bf16 [B, H].
         ``residual`` (bf16 [B, H], may be ``out`` itself) is added before the one
@@ -302,8 +322,5 @@ class OprojAllReduce:
             d.world, d.rank = self.symm.world, self.symm.rank
             for r, p in enumerate(self.symm.ptrs):
                 d.symm[r] = p
-            d.epoch = self.symm.next_epoch()
-        s = stream if stream is not None else torch.cuda.current_stream(x.device)
-        _check(_lib().ofb_oproj_allreduce(ctypes.byref(d), ctypes.c_void_p(s.cuda_stream)),
-               "ofb_oproj_allreduce")
-        return out if parts is None else parts
+            d.epoch = 1                  # the real epoch is taken at launch
+        return d, (out if parts is None else parts)

@@ -279,6 +279,7 @@ class TensorParallelLlama:
             self.w_o, self.w_d = w_o, w_d
         self.max_batch = max_batch
         self._bufs = None
+        self._k6_descs = {}          # (B, x parity) -> per layer prebuilt K6 descriptors
         self.last_hidden = None
 
     def layer_weights(self, l: int) -> dict:
@@ -318,19 +319,42 @@ class TensorParallelLlama:
                           "v_new": mk(L, B, hkv, 128), "act": mk(L, B, self.inter),
                           "h": mk(B, self.hidden), "x": [mk(B, self.hidden), mk(B, self.hidden)],
                           "a": mk(L, B, self.hidden), "a2": mk(L, B, self.hidden),
-                          "gu": mk(B, 2 * self.inter),
+                          "gu": mk(B, 2 * self.inter), "attn_out": mk(L, B, hq, 128),
                           # per hidden tile, per row: sum of x^2 (the fused RMSNorms)
                           "ss": torch.empty((self.hidden // 128, self.max_batch), dtype=torch.float32,
                                             device=dev)}
         return self._bufs
 
-    def _reduce(self, proj, w, x_all, l, x, h, stream, ss=None):
-        """x += sum over ranks of x_all[l] @ w[l]^T (C1).  K6 folds the residual
-        add into its epilogue (and leaves the new x's row sums of squares in
-        ``ss``); the NCCL arm projects into ``h``, all-reduces it and adds."""
-        if self.c1 == "k6":
-            proj(x_all, l, out=x, stream=stream, residual=x, ss_out=ss)
-            return
+    def _k6_plan(self, B: int, bufs: dict, parity: int) -> list:
+        """Per layer, the four K6 descriptors of the fused step, built (and
+        validated) once per batch size and residual buffer: a step then only
+        patches this step's pool tables / positions into the q/k/v one and
+        launches - the per-call Python of building them was ~70 % of the step's
+        host enqueue (5.4 ms at 4K context, close to the 6.4 ms GPU step)."""
+        key = (B, parity, id(bufs))
+        plan = self._k6_descs.get(key)
+        if plan is not None:
+            return plan
+        x = bufs["x"][parity]
+        q, kn, vn, ss = bufs["q"], bufs["k_new"], bufs["v_new"], bufs["ss"]
+        nq, nk = self.shard.local_q * 128, self.shard.local_kv * 128
+        kv0 = {"pool": 1, "tables": 1, "positions": 1, "host_slabs": 0, "max_blocks": 1, "part": 1,
+               "block_bytes": self.ex.shape.block_bytes}      # patched every step
+        plan = []
+        for l in range(self.ex.shape.num_layers):
+            qkv, _ = self.qkv_proj.prepare(x, l, ss_in=ss, eps=self.eps, kv_append=kv0,
+                                           parts=[q[l].view(B, nq), kn[l].view(B, nk), vn[l].view(B, nk)])
+            o, _ = self.oproj.prepare(bufs["attn_out"], l, out=x, residual=x, ss_out=ss)   # C1
+            gu, _ = self.gu_proj.prepare(x, l, out=bufs["act"][l], ss_in=ss, eps=self.eps, swiglu=True)
+            dn, _ = self.down.prepare(bufs["act"], l, out=x, residual=x, ss_out=ss)
+            plan.append((qkv, o, gu, dn))
+        self._k6_descs = {key: plan}
+        return plan
+
+    def _reduce(self, w, x_all, l, x, h):
+        """The cuBLAS + NCCL arm of C1: x += sum over ranks of x_all[l] @ w[l]^T
+        (projected into ``h``, all-reduced, added).  The K6 arm does this in one
+        kernel with the residual add in its epilogue (``_k6_plan``)."""
         torch.matmul(x_all[l].reshape(h.shape[0], -1), w[l].t(), out=h)
         if self.world > 1:
             import torch.distributed as dist
@@ -361,7 +385,7 @@ class TensorParallelLlama:
             raise ValueError("batch exceeds max_batch")
         bufs = self._buffers(B)
         q, kn, vn = bufs["q"], bufs["k_new"], bufs["v_new"]
-        desc, keep = ex.prepare_step(batch, {"q": q, "k_new": kn, "v_new": vn})
+        desc, keep = ex.prepare_step(batch, {"q": q, "k_new": kn, "v_new": vn, "out": bufs["attn_out"]})
         k6 = self.c1 == "k6"
         # K6 writes the resident rows' new K/V straight into the pool (K3 folded
         # into the q/k/v epilogue); the runtime appends only host-slab rows
@@ -374,24 +398,27 @@ class TensorParallelLlama:
         nq, nk = self.shard.local_q * 128, self.shard.local_kv * 128
         a_all, a2_all, gu = bufs["a"], bufs["a2"], bufs["gu"]
         ss = bufs["ss"]
-        kv_base = {"pool": desc.kv_pool, "positions": desc.positions, "max_blocks": desc.max_blocks,
-                   "part": 1, "block_bytes": ex.shape.block_bytes}
         bt_layer = B * desc.max_blocks * 4
+        sh = stream.cuda_stream
+        plan = None
         if k6:   # the first layer's fused RMSNorm: row sums of squares of the embeddings
             from . import _native
 
             _native.check(_native.load().ofb_row_sumsq(x.data_ptr(), ss.data_ptr(), B, self.hidden,
-                                                       self.max_batch, stream.cuda_stream), "ofb_row_sumsq")
+                                                       self.max_batch, sh), "ofb_row_sumsq")
+            plan = self._k6_plan(B, bufs, ex.steps % 2)
         ex.runtime.step_begin(desc, stream)
         try:
             for l in range(L):
                 a = a_all[l]
                 if k6:     # RMSNorm(x) . W_qkv^T for this rank's heads in one launch, into their
                     # buffers, the new token's K/V also into its pool slot (resident rows)
-                    kv = dict(kv_base, tables=desc.block_tables + l * bt_layer,
-                              host_slabs=desc.host_slabs_dev + l * B * 8)
-                    self.qkv_proj(x, l, stream=stream, ss_in=ss, eps=self.eps, kv_append=kv,
-                                  parts=[q[l].view(B, nq), kn[l].view(B, nk), vn[l].view(B, nk)])
+                    qd = plan[l][0]
+                    qd.kv_pool, qd.kv_max_blocks = desc.kv_pool, desc.max_blocks
+                    qd.kv_tables = desc.block_tables + l * bt_layer
+                    qd.kv_positions = desc.positions
+                    qd.kv_host_slabs = desc.host_slabs_dev + l * B * 8
+                    self.qkv_proj.launch(qd, sh)
                 else:
                     self._rmsnorm(x, self.norm[0], a, stream)
                     w = self.w_qkv[l]
@@ -399,18 +426,18 @@ class TensorParallelLlama:
                     torch.matmul(a, w[nq:nq + nk].t(), out=kn[l].view(B, nk))
                     torch.matmul(a, w[nq + nk:].t(), out=vn[l].view(B, nk))
                 ex.runtime.step_layers(1)                    # K3 + K2 wait + K1 of layer l
-                self._reduce(getattr(self, "oproj", None), getattr(self, "w_o", None), out, l, x, h,
-                             stream, ss)                     # x += o_proj(attn) (C1)
-                if k6:     # act = silu(gate) * up of RMSNorm(x) . W_gu^T, one launch
-                    self.gu_proj(x, l, out=bufs["act"][l], stream=stream, ss_in=ss, eps=self.eps,
-                                 swiglu=True)
-                else:
-                    a2 = a2_all[l]
-                    self._rmsnorm(x, self.norm[1], a2, stream)
-                    torch.matmul(a2, self.w_gu[l].t(), out=gu)
-                    self._silu_mul(gu, bufs["act"][l], stream)
-                self._reduce(getattr(self, "down", None), getattr(self, "w_d", None), bufs["act"],
-                             l, x, h, stream, ss)            # x += down(act) (C1)
+                if k6:
+                    self.oproj.launch(plan[l][1], sh)         # x += o_proj(attn) (C1)
+                    self.gu_proj.launch(plan[l][2], sh)       # act = silu(gate) * up of RMSNorm(x) . W_gu^T
+                    self.down.launch(plan[l][3], sh)          # x += down(act) (C1)
+                    continue
+                # cuBLAS + NCCL arm: standalone glue between the projections
+                self._reduce(self.w_o, out, l, x, h)                 # x += o_proj(attn) (C1)
+                a2 = a2_all[l]
+                self._rmsnorm(x, self.norm[1], a2, stream)
+                torch.matmul(a2, self.w_gu[l].t(), out=gu)
+                self._silu_mul(gu, bufs["act"][l], stream)
+                self._reduce(self.w_d, bufs["act"], l, x, h)         # x += down(act) (C1)
         except BaseException:
             ex.runtime.step_abort()
             raise

@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--layers", type=int, default=80)
     ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--c1", default="k6")
+    ap.add_argument("--host-profile", action="store_true",
+                    help="cProfile one step's host-side enqueue (top functions)")
     ap.add_argument("--profile-last", action="store_true",
                     help="cudaProfilerStart/Stop around the last step (ncu --profile-from-start off)")
     args = ap.parse_args()
@@ -45,11 +47,24 @@ def main():
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     torch.cuda.synchronize()
     evs[0].record()
+    import time
+    host_ms = []
     for i in range(args.steps):
         if args.profile_last and i == args.steps - 1:
             torch.cuda.synchronize()
             torch.cuda.profiler.start()
-        dec.step(batch, x)
+        t0 = time.perf_counter()
+        if args.host_profile and i == args.steps - 1:
+            import cProfile
+            import pstats
+            prof = cProfile.Profile()
+            prof.enable()
+            dec.step(batch, x)
+            prof.disable()
+            pstats.Stats(prof).sort_stats("tottime").print_stats(15)
+        else:
+            dec.step(batch, x)
+        host_ms.append((time.perf_counter() - t0) * 1e3)
         if args.profile_last and i == args.steps - 1:
             torch.cuda.synchronize()
             torch.cuda.profiler.stop()
@@ -59,7 +74,7 @@ def main():
     torch.cuda.synchronize()
     ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
     print(json.dumps({"tp": args.tp, "batch": B, "prompt": args.prompt, "c1": args.c1,
-                      "weight_bytes": dec.weight_bytes, "step_ms": ms}))
+                      "weight_bytes": dec.weight_bytes, "step_ms": ms, "host_enqueue_ms": host_ms}))
     dec.close()
     ex.close()
 
