@@ -77,7 +77,8 @@ def main():
     for name, b, k, h in SHAPES:
         if only and name != only:
             continue
-        layers = max(4, (512 << 20) // (h * k * 2))
+        # weights rotate past L2 unless --l2-resident (one layer: W stays in L2)
+        layers = 1 if "--l2-resident" in sys.argv else max(4, (512 << 20) // (h * k * 2))
         w = (torch.randn((layers, h, k), device=dev) * k ** -0.5).to(torch.bfloat16)
         x = torch.randn((layers, b, k), device=dev).to(torch.bfloat16)
         op = OprojAllReduce(w, b)
