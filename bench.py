@@ -1147,6 +1147,9 @@ def run_cfg4_serve(args):
                                  "measured_ms_full_batch_median": full_ms,
                                  "full_batch_steps": len(full),
                                  "achieved_frac": roof_ms / full_ms,
+                                 # per-GPU rates over the full-batch median step
+                                 "hbm_gbs_per_gpu": hbm_alg / (full_ms * 1e-3) / 1e9,
+                                 "host_link_gbs_per_gpu": host_alg / (full_ms * 1e-3) / 1e9,
                                  "first_step_ms": gpu_ms[0]},
                "clocks": clocks.summary()}
         if "wall_us" in steps[0]["payload"]:
