@@ -283,3 +283,98 @@ def test_rmsnorm_and_silu_mul_glue_match_fp32(rows, hidden):
     _native.check(lib.ofb_silu_mul(gu.data_ptr(), act.data_ptr(), rows, inter, s), "ofb_silu_mul")
     want = F.silu(gu[:, :inter].float()) * gu[:, inter:].float()
     torch.testing.assert_close(act.float(), want, rtol=2e-2, atol=1e-2)
+
+
+def _tp2_worker(rank, port, q):
+    """One rank of a 2-way tensor-parallel whole-decoder step (gloo for the
+    control plane; both processes share the box's GPU, so K6's exchange runs
+    over CUDA IPC between the two contexts)."""
+    import os
+
+    import torch.distributed as dist
+
+    from paper_2601_10729_b200.executor import B200Executor, ModelShape
+    from paper_2601_10729_b200.tp import HeadShard, TensorParallelLlama
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        torch.cuda.set_device(0)
+        L, B = 2, 3
+        shard = HeadShard(rank, 2, 8, 2)
+        ex = B200Executor(ModelShape(L, shard.local_q, shard.local_kv), device_blocks=L * B * 40 + 2 * B * 40 + 64,
+                          host_blocks=L * B * 40 + 64, staging_slots=2, seed=11 + rank)
+        dec = TensorParallelLlama(ex, shard, 256, 512, c1="k6", group=dist.group.WORLD, seed=0, max_batch=B)
+        batch = _batch(B)
+        rows = ((1, 0), (1, 1), (0, 1))               # host-resident slabs too (K2 + the runtime append)
+        ex.install(batch, PlacementMatrix(tuple(r.id for r in batch), L, rows))
+        g = torch.Generator(device=ex.device)
+        g.manual_seed(99)                             # the same embeddings on both ranks
+        res = []
+        for _ in range(2):
+            x_in = torch.randn((B, 256), generator=g, device=ex.device).to(torch.bfloat16)
+            out = dec.step(batch, x_in)
+            torch.cuda.synchronize()
+            # numpy, not tensors: CPU tensors cross the queue by shared-memory handles
+            # that die with this process
+            npf = lambda t: t.float().cpu().numpy().copy()  # noqa: E731
+            res.append({"x_in": npf(x_in), "out": out.view(torch.int16).cpu().numpy().copy(),
+                        "attn": npf(ex.last_output), "q": npf(ex.last_inputs["q"]),
+                        "w": [{k: npf(v) for k, v in dec.layer_weights(l).items()} for l in range(L)]})
+            for r in batch:
+                r.record_generated_token()
+        dec.close()
+        ex.close()
+        q.put((rank, res))
+    except Exception as exc:  # surfaced in the parent
+        import traceback
+
+        q.put((rank, f"error: {exc!r}\n{traceback.format_exc()}"))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_whole_decoder_step_matches_the_unsharded_chain():
+    """N = 2 KV-head shards of one decoder (two processes, one GPU): both ranks end
+    every step with bit-identical hidden states, equal to an fp32 restatement of
+    the UNSHARDED layer chain - q/k/v of each rank's heads, the o-projection and
+    the MLP partials summed over the ranks by K6's exchange (with the residual add,
+    the fused RMSNorms' row sums of squares and SwiGLU folded in)."""
+    import multiprocessing as mp
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_tp2_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in (0, 1):
+        assert not isinstance(res[r], str), res[r]
+    def tensors(s):
+        t = {k: torch.from_numpy(v) for k, v in s.items() if k != "w"}
+        t["out"] = t["out"].view(torch.bfloat16)
+        t["w"] = [{k: torch.from_numpy(v) for k, v in wl.items()} for wl in s["w"]]
+        return t
+
+    for step in range(2):
+        s0, s1 = tensors(res[0][step]), tensors(res[1][step])
+        assert torch.equal(s0["out"], s1["out"]), f"ranks disagree at step {step}"
+        x = s0["x_in"]
+        B = x.shape[0]
+        for l in range(len(s0["w"])):
+            a = _rms(x)
+            for s in (s0, s1):        # each rank's q projection of its own heads
+                torch.testing.assert_close(s["q"][l].reshape(B, -1), a @ s["w"][l]["q"].t(),
+                                           rtol=3e-2, atol=3e-2)
+            x = x + sum(s["attn"][l].reshape(B, -1) @ s["w"][l]["o"].t() for s in (s0, s1))
+            a = _rms(x)
+            x = x + sum((F.silu(a @ s["w"][l]["gate"].t()) * (a @ s["w"][l]["up"].t())) @ s["w"][l]["down"].t()
+                        for s in (s0, s1))
+        torch.testing.assert_close(s0["out"].float(), x, rtol=5e-2, atol=5e-2)
