@@ -378,3 +378,66 @@ def test_two_rank_whole_decoder_step_matches_the_unsharded_chain():
             x = x + sum((F.silu(a @ s["w"][l]["gate"].t()) * (a @ s["w"][l]["up"].t())) @ s["w"][l]["down"].t()
                         for s in (s0, s1))
         torch.testing.assert_close(s0["out"].float(), x, rtol=5e-2, atol=5e-2)
+
+
+def _tp2_engine_worker(rank, port, q):
+    """One rank of a 2-way TP deployment driven by the reference serving loop."""
+    import os
+
+    import torch.distributed as dist
+
+    from paper_2601_10729_b200.executor import B200Executor, ModelShape
+    from paper_2601_10729_b200.tp import HeadShard, TensorParallelExecutor, TensorParallelLlama
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        torch.cuda.set_device(0)
+        prof, slo, trace, cfg = _toy_engine()
+        shard = HeadShard(rank, 2, 8, 2)
+        ex = B200Executor.for_trace(trace, prof, shape=ModelShape(4, shard.local_q, shard.local_kv), max_batch=3)
+        dec = TensorParallelLlama(ex, shard, 256, 512, group=dist.group.WORLD, max_batch=3)
+        tex = TensorParallelExecutor(dec, group=dist.group.WORLD)
+        policy = make_policy(PolicyKind.ORBIT, prof, slo, max_batch=3, token_cap=cfg.batch_token_cap)
+        log = Simulation(trace, policy, prof, slo, cfg, executor=tex).execute()
+        steps = [r for r in log if r["kind"] == "step"]
+        hidden = dec.last_hidden.view(torch.int16).cpu().numpy().copy()
+        ok = bool(steps) and all(r["payload"]["measured_us"] > 0 for r in steps) and tex.steps == len(steps)
+        tex.close()
+        q.put((rank, (_strip(log), hidden, ok)))
+    except Exception as exc:  # surfaced in the parent
+        import traceback
+
+        q.put((rank, f"error: {exc!r}\n{traceback.format_exc()}"))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_tp_executor_under_engine():
+    """Two ranks (two processes, one GPU) each run the reference serving loop over
+    their KV-head shard: plans are recomputed per rank (C2, digest-checked), the
+    measured step is the max over ranks, and both ranks' event logs equal the
+    executor-less model run; the last hidden states are bit-identical."""
+    import multiprocessing as mp
+    import socket
+
+    prof, slo, trace, cfg = _toy_engine()
+    model = Simulation(trace, make_policy(PolicyKind.ORBIT, prof, slo, max_batch=3,
+                                          token_cap=cfg.batch_token_cap), prof, slo, cfg).execute()
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_tp2_engine_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in (0, 1):
+        assert not isinstance(res[r], str), res[r]
+        log, _hidden, ok = res[r]
+        assert ok and log == model, f"rank {r}: decisions differ from the model run"
+    assert (res[0][1] == res[1][1]).all(), "ranks' hidden states differ"
