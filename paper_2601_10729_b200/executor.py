@@ -375,7 +375,7 @@ class B200Executor:
         g.manual_seed(self.seed * 7919 + (self.steps if step is None else step) + 1)
         L, hq, hkv = self.shape.num_layers, self.shape.num_q_heads, self.shape.num_kv_heads
         mk = lambda h: torch.randn((L, B, h, HEAD_DIM), generator=g, device=self.device,  # noqa: E731
-                                   dtype=torch.float32).to(torch.bfloat16)
+                                   dtype=torch.bfloat16)
         return {"q": mk(hq), "k_new": mk(hkv), "v_new": mk(hkv)}
 
     def prepare_step(self, batch: list[RequestState], inputs: dict | None = None):
