@@ -126,6 +126,34 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint6
       : "memory");
 }
 
+// One 64-element K chunk: four K=16 MMAs (+32 B along the swizzle atom each) in
+// one asm block, so the single issuing thread spends a handful of instructions
+// per chunk (at decode shapes the whole W tile often lands at once and the MMA
+// issue is what remains after the last byte)
+__device__ __forceinline__ void umma_chunk(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                           uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p, t;\nsetp.ne.b32 p, %4, 0;\nsetp.eq.b32 t, 0, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %5, %6, %3, t;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %7, %8, %3, t;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %9, %10, %3, t;\n}\n"
+      ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate),
+        "l"(adesc + 2), "l"(bdesc + 2), "l"(adesc + 4), "l"(bdesc + 4), "l"(adesc + 6), "l"(bdesc + 6)
+      : "memory");
+}
+
+// one lane of a converged warp (elect.sync): the MMA warp runs its loop
+// converged and issues from the elected lane, so ptxas emits the tcgen05
+// instructions without a per-instruction divergence loop
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .b32 rx;\n.reg .pred px;\nelect.sync rx|px, %1;\n@px mov.u32 %0, 1;\n}\n"
+      : "+r"(pred) : "r"(0xFFFFFFFFu));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                ::"r"(smem_u32(bar)) : "memory");
@@ -267,34 +295,62 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
   if (a.splits > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   if (tr) tr[1] = globaltimer();
 
-  if (warp == 0 && lane == 0) {
-    // TMA producer: the first stages' W loads are in flight (above)
+  if (warp == 0) {
+    // TMA producer (the whole warp, converged; one elected lane issues): the
+    // first stages' W loads are in flight (above)
     pdl_wait();
-    for (int i = 0; i < pre; ++i)
-      tma_load_3d(smem + i * stage_bytes + stage_w, &xmap, &full_bar[i], (c0 + i) * kChunkK, 0, a.x_layer);
+    if (elect_one())
+      for (int i = 0; i < pre; ++i)
+        tma_load_3d(smem + i * stage_bytes + stage_w, &xmap, &full_bar[i], (c0 + i) * kChunkK, 0, a.x_layer);
+    __syncwarp();
+    // refills: chunk i >= pre = stages reuses stage i % stages once its MMAs read it
+    int s = 0;
+    uint32_t ph = 0;
     for (int i = pre; i < nchunks; ++i) {
-      const int s = i % a.stages, round = i / a.stages;
-      mbar_wait(&empty_bar[s], (round - 1) & 1);
-      uint8_t* sw = smem + s * stage_bytes;
-      mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
-      tma_load_4d(sw, &wmap, &full_bar[s], 0, 0, c0 + i, a.layer * a.tiles + tile);
-      tma_load_3d(sw + stage_w, &xmap, &full_bar[s], (c0 + i) * kChunkK, 0, a.x_layer);
+      mbar_wait(&empty_bar[s], ph);
+      if (elect_one()) {
+        uint8_t* sw = smem + s * stage_bytes;
+        mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
+        tma_load_4d(sw, &wmap, &full_bar[s], 0, 0, c0 + i, a.layer * a.tiles + tile);
+        tma_load_3d(sw + stage_w, &xmap, &full_bar[s], (c0 + i) * kChunkK, 0, a.x_layer);
+      }
+      __syncwarp();
+      if (++s == a.stages) {
+        s = 0;
+        ph ^= 1u;
+      }
     }
-  } else if (warp == 1 && lane == 0) {
-    // MMA issuer: D[128 x npad] (TMEM) += W_tile[128 x 64] . X[npad x 64]^T per stage
+  } else if (warp == 1) {
+    // MMA issuer (the whole warp, converged; one elected lane issues):
+    // D[128 x npad] (TMEM) += W_tile[128 x 64] . X[npad x 64]^T per stage
     const uint32_t idesc = umma_idesc_bf16(kTileM, a.npad);
+    // descriptors advance by the stage size (address field = byte address >> 4;
+    // shared addresses < 256 KiB never carry out of it); no per-chunk division
+    const uint64_t ad0 = sw128_kmajor_desc(smem_u32(smem)), bd0 = sw128_kmajor_desc(smem_u32(smem + stage_w));
+    const uint64_t dstep = static_cast<uint64_t>(stage_bytes >> 4);
+    uint64_t ad = ad0, bd = bd0;
+    int s = 0;
+    uint32_t ph = 0;
     for (int i = 0; i < nchunks; ++i) {
-      const int s = i % a.stages, round = i / a.stages;
-      mbar_wait(&full_bar[s], round & 1);
+      mbar_wait(&full_bar[s], ph);
       tc_fence_after();
-      const uint64_t ad = sw128_kmajor_desc(smem_u32(smem + s * stage_bytes));
-      const uint64_t bd = sw128_kmajor_desc(smem_u32(smem + s * stage_bytes + stage_w));
-#pragma unroll
-      for (int k = 0; k < kChunkK / 16; ++k)   // +32 B per K=16 step inside the swizzle atom
-        umma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
-      umma_commit(&empty_bar[s]);              // frees the stage once these MMAs have read it
+      if (elect_one()) {
+        umma_chunk(tmem, ad, bd, idesc, i > 0 ? 1u : 0u);
+        umma_commit(&empty_bar[s]);            // frees the stage once these MMAs have read it
+      }
+      __syncwarp();
+      if (++s == a.stages) {
+        s = 0;
+        ph ^= 1u;
+        ad = ad0;
+        bd = bd0;
+      } else {
+        ad += dstep;
+        bd += dstep;
+      }
     }
-    umma_commit(&acc_bar);
+    if (elect_one()) umma_commit(&acc_bar);
+    __syncwarp();
   }
   __syncwarp();
 
