@@ -48,6 +48,18 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
                ::"r"(smem_u32(bar)) : "memory");
 }
 
+// One lane of a converged warp (elect.sync).  Producer / MMA warps run their
+// loops converged and issue TMA / tcgen05 from the elected lane: issued from a
+// lone lane instead, ptxas wraps every such instruction in an ELECT /
+// BRA.U.ANY divergence loop (~5 instructions each on a single-thread critical path).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .b32 rx;\n.reg .pred px;\nelect.sync rx|px, %1;\n@px mov.u32 %0, 1;\n}\n"
+      : "+r"(pred) : "r"(0xFFFFFFFFu));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"

@@ -197,18 +197,20 @@ __device__ __forceinline__ void paged_gqa_decode_body(const CUtensorMap& kv_map,
 
   if (warp == kW) {
     // ---------------------------------------------------------- producer
-    if (lane == 0) {
-      const int last_blk = (seq - 1) / kBlockTokens;   // block of this step's token
-      for (int i = 0; i < n; ++i) {
-        const int st = i % kS;
-        if (i >= kS) mbar_wait(&empty[st], ((i / kS) - 1) & 1);
-        if (a.kv_ready == 2 && b_begin + i == last_blk) pdl_wait();   // the token's K/V is the predecessor's
+    // (the whole warp, converged; the elected lane issues)
+    const int last_blk = (seq - 1) / kBlockTokens;   // block of this step's token
+    for (int i = 0; i < n; ++i) {
+      const int st = i % kS;
+      if (i >= kS) mbar_wait(&empty[st], ((i / kS) - 1) & 1);
+      if (a.kv_ready == 2 && b_begin + i == last_blk) pdl_wait();   // the token's K/V is the predecessor's
+      if (elect_one()) {
         const int row = (blk_ids[i] * a.hkv + kvh) * kTileRows;
         uint8_t* dst = ring + (size_t)st * kHeadBlockBytes;
         mbar_arrive_expect_tx(&full[st], kHeadBlockBytes);
         tma_load_2d(dst, &kv_map, &full[st], 0, row);
         tma_load_2d(dst + kHeadBlockBytes / 2, &kv_map, &full[st], 64, row);
       }
+      __syncwarp();
     }
   } else {
     // ---------------------------------------------------------- consumers
@@ -700,33 +702,47 @@ int attention_cluster_slots(int* slots);
 int attention_cluster_plan(int batch, int hkv, int max_seq_len, const int* slots, int* C, int* P,
                            int* bps, int* stages);
 
-// Fitted on tools/k1_variant_sweep.py (profiles/r02_k1_variants.md): the
-// cluster kernel wins when a pair gets a whole cluster and its CTAs stay short
-// (<= 4 (request, KV head) pairs, <= 40 blocks per CTA), and on tiny contexts
-// (<= 64 blocks) with <= 8 pairs; with more pairs the GPC packing of clusters
-// (7 x 16, 15 x 8, 33 x 4 CTAs on 148 SMs) leaves each pair too few CTAs.
+// In-step choice between the split kernel (global ticket + combine) and the
+// cluster kernel (DSMEM combine), from the all-resident step probe
+// (tools/small_step_probe.py, profiles/r02_k1_issue_loops.md): the cluster kernel
+// wins with one cluster of <= 4 CTAs per (request, KV head) (8B / 70B at B 4-16,
+// up to 8K) or one cluster with <= 20 blocks per CTA, and with >= 5 clusters per
+// pair (the 70B TP8 shard at B = 1, 8K-32K); 2-4 clusters per pair lose 0.3-0.7 us.
+static bool cluster_pick(int C, int P, int bps) {
+  return (P == 1 && (C <= 4 || bps <= 20)) || (P >= 5 && bps <= 40);
+}
+
 bool cluster_preferred(int batch, int hq, int hkv, int max_seq_len) {
   (void)hq;
   int slots[5], C, P, bps, stages;
   if (attention_cluster_slots(slots) != 0) return false;
   if (attention_cluster_plan(batch, hkv, max_seq_len, slots, &C, &P, &bps, &stages) != 0)
     return false;
-  const long pairs = (long)batch * hkv;
-  const long nblk = (max_seq_len + kBlockTokens - 1) / kBlockTokens;
-  return (pairs <= 4 && bps <= 40) || (pairs <= 8 && nblk <= 64);
+  return cluster_pick(C, P, bps);
+}
+
+// Standalone launches with <= 8 blocks per CTA of a picked cluster plan (1K
+// contexts): the cluster kernel beat split2 there (4.9-5.4 vs 5.9-6.4 us).
+static bool cluster_short(int batch, int hkv, int max_seq_len) {
+  int slots[5], C, P, bps, stages;
+  if (attention_cluster_slots(slots) != 0) return false;
+  if (attention_cluster_plan(batch, hkv, max_seq_len, slots, &C, &P, &bps, &stages) != 0)
+    return false;
+  return cluster_pick(C, P, bps) && bps <= 8;
 }
 
 // Auto.  A standalone launch (the public entry point, which waits for its
 // predecessor before streaming) with a one-wave, multi-split grid over <= 16
-// pairs uses split2: the separate combine kernel beat both the last-CTA combine
-// and the cluster kernel on every such shape (profiles/r02_k1_split2.md).  Inside a
-// step one kernel per layer is kept (split / cluster): the later layers stream
-// their KV before the PDL wait, and a combine kernel between two layers cost
-// 0.5 us per layer there (the next cluster K1 places its clusters around it).
+// pairs uses split2 (the separate combine kernel), unless a short cluster plan
+// applies (profiles/r02_k1_split2.md, r02_k1_issue_loops.md).  Inside a step one
+// kernel per layer is kept (split / cluster): the later layers stream their KV
+// before the PDL wait, and a combine kernel between two layers cost 0.5 us per
+// layer there (the next cluster K1 places its clusters around it).
 static int pick_variant(int batch, int hq, int hkv, int max_seq_len, bool standalone = false) {
   const int v = k1_variant();
   if (v != 2) return v;
   if (standalone && attn_init_once() == cudaSuccess && hkv > 0 && hq % hkv == 0) {
+    if (cluster_short(batch, hkv, max_seq_len)) return 3;
     const AttnPlan p = plan_splits(batch, hq, hkv, max_seq_len, g_num_sms, g_attn_occupancy);
     const long ctas = (long)p.max_splits * hkv * batch;
     // <= 16 (request, KV head) pairs: beyond that the last-CTA combine spreads over

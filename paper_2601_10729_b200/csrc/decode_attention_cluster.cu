@@ -39,6 +39,7 @@ constexpr int kCWarps = 4;                       // consumer warps
 constexpr int kCThreads = (kCWarps + 1) * 32;    // + producer warp
 constexpr int kCMaxStages = 24;
 constexpr int kCMinStages = 5;                   // the 4-warp merge scratch overlays the ring
+static_assert(kCMinStages > 4, "the consumer loop wraps the ring at most once per step");
 constexpr int kCMaxCluster = 16;
 constexpr int kCMaxBps = 256;
 constexpr size_t kCCounterBytes = 65536;         // shared counter region (split kernel layout)
@@ -157,29 +158,44 @@ paged_gqa_decode_cluster_kernel(const __grid_constant__ CUtensorMap kv_map, cons
   WarpAttnState st;
   st.reset();
   if (warp == kCWarps) {
-    if (lane == 0) {
-      for (int i = 0; i < n; ++i) {
-        const int s = i % a.stages;
-        if (i >= a.stages) mbar_wait(&empty[s], ((i / a.stages) - 1) & 1);
+    // producer: the whole warp, converged; the elected lane issues
+    int s = 0;
+    uint32_t ph = 0;
+    for (int i = 0; i < n; ++i) {
+      if (i >= a.stages) mbar_wait(&empty[s], ph ^ 1u);
+      if (elect_one()) {
         const int row = (tl->blk_ids[i] * a.hkv + kvh) * kTileRows;
         uint8_t* dst = ring + (size_t)s * kHeadBlockBytes;
         mbar_arrive_expect_tx(&full[s], kHeadBlockBytes);
         tma_load_2d(dst, &kv_map, &full[s], 0, row);
         tma_load_2d(dst + kHeadBlockBytes / 2, &kv_map, &full[s], 64, row);
       }
+      __syncwarp();
+      if (++s == a.stages) {
+        s = 0;
+        ph ^= 1u;
+      }
     }
   } else {
     if (early) pdl_wait();
     uint32_t qa[8][4];
     load_q_frag(qa, a.q + ((size_t)req * a.hq + qh0) * kHeadDim, g, lane);
+    // stage / phase advance incrementally (stages >= kCMinStages > kCWarps: at most
+    // one wrap per step) - no division by the runtime ring depth per tile
+    int s = warp;
+    uint32_t ph = 0;
     for (int i = warp; i < n; i += kCWarps) {
-      const int s = i % a.stages;
-      mbar_wait(&full[s], (i / a.stages) & 1);
+      mbar_wait(&full[s], ph);
       if (tr && i == 0 && lane == 0) tr[2] = cl_gtimer();
       const int valid = min(kBlockTokens, seq - (b_begin + i) * kBlockTokens);
       attend_tile(st, qa, ring + (size_t)s * kHeadBlockBytes, valid, a.scale_log2, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      s += kCWarps;
+      if (s >= a.stages) {
+        s -= a.stages;
+        ph ^= 1u;
+      }
     }
   }
   __syncthreads();   // ring drained

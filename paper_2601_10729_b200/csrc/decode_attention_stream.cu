@@ -196,9 +196,9 @@ paged_gqa_decode_stream_kernel(const __grid_constant__ CUtensorMap kv_map, const
       const int cnt = min(32, n - i0);
       for (int j = 0; j < cnt; ++j) {
         const int rj = __shfl_sync(0xffffffffu, row_cur, j);
-        if (lane == 0) {
-          const int e = i0 + j, st = e % kSStages;
-          if (e >= kSStages) mbar_wait(&empty[st], ((e / kSStages) - 1) & 1);
+        const int e = i0 + j, st = e % kSStages;
+        if (e >= kSStages) mbar_wait(&empty[st], ((e / kSStages) - 1) & 1);
+        if (elect_one()) {   // converged warp, elected lane issues
           uint8_t* dst = ring + (size_t)st * kHeadBlockBytes;
           mbar_arrive_expect_tx(&full[st], kHeadBlockBytes);
           tma_load_2d(dst, &kv_map, &full[st], 0, rj);

@@ -143,17 +143,6 @@ __device__ __forceinline__ void umma_chunk(uint32_t tmem_d, uint64_t adesc, uint
       : "memory");
 }
 
-// one lane of a converged warp (elect.sync): the MMA warp runs its loop
-// converged and issues from the elected lane, so ptxas emits the tcgen05
-// instructions without a per-instruction divergence loop
-__device__ __forceinline__ bool elect_one() {
-  uint32_t pred = 0;
-  asm volatile(
-      "{\n.reg .b32 rx;\n.reg .pred px;\nelect.sync rx|px, %1;\n@px mov.u32 %0, 1;\n}\n"
-      : "+r"(pred) : "r"(0xFFFFFFFFu));
-  return pred != 0;
-}
-
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                ::"r"(smem_u32(bar)) : "memory");

@@ -1,6 +1,7 @@
 """All-resident decode steps at small batch (the cfg3 regime): device time per
-step for the 8B shape and the 70B TP8 rank shard (8 q / 1 KV head), B in {1, 4},
-4K and 16K context, stream-launched and pipelined: the per-layer K1 cost inside
+step for the 8B shape and the 70B TP8 rank shard (8 q / 1 KV head), B in {1, 4}
+(--batches 1,2,4), 4K and 16K context (--contexts 1024,4096),
+stream-launched and pipelined: the per-layer K1 cost inside
 a step (K1 of a layer without a fetch streams its KV before the PDL wait).
 Run once as is and once with OFB_PDL=0 to see what programmatic dependent launch
 (+ kv_ready KV streaming before the wait) buys when each layer is short."""
@@ -17,8 +18,13 @@ from paper_2601_10729_b200.executor import B200Executor, ModelShape  # noqa: E40
 
 import itertools  # noqa: E402
 
+def _arg(flag, default):
+    return [int(v) for v in sys.argv[sys.argv.index(flag) + 1].split(",")] if flag in sys.argv else default
+
+
 for (name, shape), B, ctx in itertools.product(
-        [("8B", ModelShape(32, 32, 8)), ("70B-TP8-shard", ModelShape(32, 8, 1))], (1, 4), (4096, 16384)):
+        [("8B", ModelShape(32, 32, 8)), ("70B-TP8-shard", ModelShape(32, 8, 1))],
+        _arg("--batches", (1, 4)), _arg("--contexts", (4096, 16384))):
     cap = -(-(ctx + 64 + 1) // 16)
     batch = [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=ctx, target_output_tokens=64)
              for i in range(B)]
