@@ -384,6 +384,22 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
     }
     if (a.splits == 1) __syncthreads();   // else the cluster barrier below publishes rsc
   }
+  // the residual of this thread's row for the first 32 batch columns, read while
+  // the MMAs run (an L2 round trip off the epilogue's critical path; the x loads
+  // already wait for the predecessor, so this early wait costs nothing)
+  __nv_bfloat162 res2[16];
+  const bool res_pre = a.world == 1 && a.residual && split == 0;
+  if (res_pre) {
+    pdl_wait();
+    const __nv_bfloat16* rp = a.residual + static_cast<size_t>(tile) * kTileM + warp * 32 + lane;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int b0 = 2 * j, b1 = 2 * j + 1;
+      const __nv_bfloat16 z = __float2bfloat16_rn(0.f);
+      res2[j] = __halves2bfloat162(b0 < a.batch ? rp[static_cast<size_t>(b0) * a.hidden] : z,
+                                   b1 < a.batch ? rp[static_cast<size_t>(b1) * a.hidden] : z);
+    }
+  }
   mbar_wait(&acc_bar, 0);
   if (tr) tr[2] = globaltimer();
   tc_fence_after();
@@ -441,11 +457,20 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
         if (c * 32 + j < a.batch) acc[j] *= rsc[c * 32 + j];
     }
     if (a.world == 1 && a.residual) {   // x += o_proj(attn): one rounding of x + sum
+      if (c == 0) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int b = c * 32 + j;
-        if (b < a.batch)
-          acc[j] += __bfloat162float(a.residual[static_cast<size_t>(b) * a.hidden + tile * kTileM + m]);
+        for (int j = 0; j < 16; ++j) {
+          const float2 f = __bfloat1622float2(res2[j]);
+          acc[2 * j] += f.x;
+          acc[2 * j + 1] += f.y;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int b = c * 32 + j;
+          if (b < a.batch)
+            acc[j] += __bfloat162float(a.residual[static_cast<size_t>(b) * a.hidden + tile * kTileM + m]);
+        }
       }
     }
 #pragma unroll
