@@ -357,49 +357,59 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
       if (tile * kTileM >= a.part_lo[r] && tile * kTileM < a.part_lo[r + 1]) kvsel = r - a.kv_part;
     if (kvsel != 0 && kvsel != 1) kvsel = -1;
   }
-  if (kvsel >= 0 && split == 0) {
-    // resolve every row's slot while the MMAs run (two dependent loads per row
-    // would otherwise sit on the epilogue's critical path)
-    pdl_wait();
-    const int head = (tile * kTileM - a.part_lo[a.kv_part + kvsel]) / kTileM;
-    for (int b = threadIdx.x; b < a.batch; b += kThreads) {
-      long long off = -1;
-      const int pos = a.kv_positions[b];
-      if (pos >= 0 && (!a.kv_host || a.kv_host[b] == 0)) {
-        const int blk = a.kv_tables[static_cast<size_t>(b) * a.kv_max_blocks + pos / kBlockTokens];
-        if (blk >= 0)
-          off = static_cast<long long>(blk) * a.kv_block_bytes +
-                static_cast<long long>((head * 2 + kvsel) * kBlockTokens + pos % kBlockTokens) * kRowBytes;
-      }
-      kvoff[b] = off;
-    }
-    if (a.splits == 1 && !a.ss_in) __syncthreads();   // else a barrier below publishes kvoff
-  }
-  if (a.ss_in && split == 0) {
-    pdl_wait();
-    for (int b = threadIdx.x; b < a.batch; b += kThreads) {
-      float s = 0.f;
-      for (int t = 0; t < a.ss_tiles; ++t) s += __ldcg(a.ss_in + static_cast<size_t>(t) * a.max_batch + b);
-      rsc[b] = rsqrtf(s / static_cast<float>(a.ss_tiles * kTileM) + a.eps);
-    }
-    if (a.splits == 1) __syncthreads();   // else the cluster barrier below publishes rsc
-  }
-  // the residual of this thread's row for the first 32 batch columns, read while
-  // the MMAs run (an L2 round trip off the epilogue's critical path; the x loads
-  // already wait for the predecessor, so this early wait costs nothing)
-  __nv_bfloat162 res2[16];
+  // Per-row prologue of the leader, done by warps 2-3 while the MMAs run: warps 0
+  // and 1 are the TMA producer and the MMA issuer and reach the epilogue only
+  // after their loops (the producer after its last refill), so work dealt to
+  // them by row would sit on the epilogue's critical path.  The x loads already
+  // wait for the predecessor, so the early PDL wait costs nothing.
+  //  - K3 fold: every row's pool slot (two dependent loads per row);
+  //  - fused RMSNorm (ss_in): 1/rms of every row from the producer's per-32-column
+  //    sums of squares, several lanes per row combined in a fixed shuffle order;
+  //  - the residual tile of the first 32 batch rows, staged in smem (16-byte loads).
+  __shared__ __align__(16) __nv_bfloat16 res_s[32 * kTileM];
   const bool res_pre = a.world == 1 && a.residual && split == 0;
-  if (res_pre) {
+  const bool pro = split == 0 && (kvsel >= 0 || a.ss_in || res_pre);
+  if (pro && warp >= 2) {
     pdl_wait();
-    const __nv_bfloat16* rp = a.residual + static_cast<size_t>(tile) * kTileM + warp * 32 + lane;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int b0 = 2 * j, b1 = 2 * j + 1;
-      const __nv_bfloat16 z = __float2bfloat16_rn(0.f);
-      res2[j] = __halves2bfloat162(b0 < a.batch ? rp[static_cast<size_t>(b0) * a.hidden] : z,
-                                   b1 < a.batch ? rp[static_cast<size_t>(b1) * a.hidden] : z);
+    const int pt = threadIdx.x - 64;           // 0..63
+    if (kvsel >= 0) {
+      const int head = (tile * kTileM - a.part_lo[a.kv_part + kvsel]) / kTileM;
+      for (int b = pt; b < a.batch; b += 64) {
+        long long off = -1;
+        const int pos = a.kv_positions[b];
+        if (pos >= 0 && (!a.kv_host || a.kv_host[b] == 0)) {
+          const int blk = a.kv_tables[static_cast<size_t>(b) * a.kv_max_blocks + pos / kBlockTokens];
+          if (blk >= 0)
+            off = static_cast<long long>(blk) * a.kv_block_bytes +
+                  static_cast<long long>((head * 2 + kvsel) * kBlockTokens + pos % kBlockTokens) * kRowBytes;
+        }
+        kvoff[b] = off;
+      }
+    }
+    if (a.ss_in) {
+      int lpr = 1;                              // lanes per row: a power of two <= 32
+      while (lpr < 32 && lpr * 2 * a.batch <= 64) lpr *= 2;
+      const int part = pt & (lpr - 1);
+      for (int b0 = 0; b0 < a.batch; b0 += 64 / lpr) {
+        const int b = b0 + pt / lpr;            // uniform trip count: every lane shuffles
+        float sum = 0.f;
+        if (b < a.batch)
+          for (int t = part; t < a.ss_tiles; t += lpr)
+            sum += __ldcg(a.ss_in + static_cast<size_t>(t) * a.max_batch + b);
+        for (int off = lpr >> 1; off; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+        if (b < a.batch && part == 0) rsc[b] = rsqrtf(sum / static_cast<float>(a.ss_tiles * kTileM) + a.eps);
+      }
+    }
+    if (res_pre) {
+      const int rows = a.batch < 32 ? a.batch : 32;
+      for (int i = pt; i < rows * (kTileM / 8); i += 64) {
+        const int b = i >> 4, q = i & 15;
+        *reinterpret_cast<uint4*>(res_s + b * kTileM + q * 8) = *reinterpret_cast<const uint4*>(
+            a.residual + static_cast<size_t>(b) * a.hidden + tile * kTileM + q * 8);
+      }
     }
   }
+  if (pro && a.splits == 1) __syncthreads();   // publish (else the cluster barrier below does)
   mbar_wait(&acc_bar, 0);
   if (tr) tr[2] = globaltimer();
   tc_fence_after();
@@ -457,13 +467,10 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
         if (c * 32 + j < a.batch) acc[j] *= rsc[c * 32 + j];
     }
     if (a.world == 1 && a.residual) {   // x += o_proj(attn): one rounding of x + sum
-      if (c == 0) {
+      if (c == 0) {                    // staged by the prologue (rows < min(batch, 32))
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float2 f = __bfloat1622float2(res2[j]);
-          acc[2 * j] += f.x;
-          acc[2 * j + 1] += f.y;
-        }
+        for (int j = 0; j < 32; ++j)
+          if (j < a.batch) acc[j] += __bfloat162float(res_s[j * kTileM + m]);
       } else {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
