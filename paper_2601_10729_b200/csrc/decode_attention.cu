@@ -32,7 +32,7 @@ constexpr int kConsumerWarps = 4;
 constexpr int kAttnThreads = (kConsumerWarps + 1) * 32;
 constexpr int kStages = 8;
 constexpr int kWideWarps = 8;
-constexpr int kWideStages = 16;
+constexpr int kWideStages = 24;
 constexpr int kMaxSplits = 256;
 constexpr int kMaxBlocksPerSplit = 256;
 // Split tickets live in a fixed region at the start of the workspace, sized for
@@ -176,12 +176,11 @@ __device__ __forceinline__ void paged_gqa_decode_body(const CUtensorMap& kv_map,
   }
   const int n = min(a.blocks_per_split, nblk - b_begin);
 
-  if (tid == 0) {
-    prefetch_tma_desc(&kv_map);
-    for (int s = 0; s < kS; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
+  // ring barriers initialised in parallel (thread s: stage s), not by one thread
+  if (tid == 0) prefetch_tma_desc(&kv_map);
+  if (tid < kS) {
+    mbar_init(&full[tid], 1);
+    mbar_init(&empty[tid], 1);
     fence_mbar_init();
   }
   __syncthreads();

@@ -144,12 +144,11 @@ paged_gqa_decode_cluster_kernel(const __grid_constant__ CUtensorMap kv_map, cons
   const int g = a.group;
   const int qh0 = kvh * g;
 
-  if (tid == 0) {
-    prefetch_tma_desc(&kv_map);
-    for (int s = 0; s < a.stages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
+  // ring barriers initialised in parallel (thread s: stage s), not by one thread
+  if (tid == 0) prefetch_tma_desc(&kv_map);
+  if (tid < a.stages) {
+    mbar_init(&full[tid], 1);
+    mbar_init(&empty[tid], 1);
     fence_mbar_init();
   }
   __syncthreads();

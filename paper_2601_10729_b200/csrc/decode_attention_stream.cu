@@ -137,12 +137,11 @@ paged_gqa_decode_stream_kernel(const __grid_constant__ CUtensorMap kv_map, const
     }
     if (lane == 0) rp[0] = 0;
   }
-  if (tid == 0) {
-    prefetch_tma_desc(&kv_map);
-    for (int s = 0; s < kSStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
+  // ring barriers initialised in parallel (thread s: stage s), not by one thread
+  if (tid == 0) prefetch_tma_desc(&kv_map);
+  if (tid < kSStages) {
+    mbar_init(&full[tid], 1);
+    mbar_init(&empty[tid], 1);
     fence_mbar_init();
   }
   __syncthreads();
