@@ -897,6 +897,14 @@ int ofb_oproj_allreduce(const ofb_oproj_desc* d, void* stream) {
   a.chunks = chunks;
   const int stage_bytes = kTileM * kChunkK * 2 + npad * kChunkK * 2;
   a.stages = ring_stages(npad, splits);
+  {
+    // When a CTA's whole K range fits the ring, every stage is requested at once
+    // and lands at the end together, leaving all MMAs after the last byte; a ring of
+    // 3/4 of the chunks staggers the arrivals (70B TP8 o-proj, 8 chunks per CTA:
+    // 6.25 -> 6.01 us at 6 stages; profiles/r02_k6_experiments.md)
+    const int per_cta = (chunks + splits - 1) / splits;
+    if (per_cta >= 8 && per_cta <= a.stages) a.stages = per_cta * 3 / 4;
+  }
   a.world = d->world;
   a.rank = d->rank;
   a.max_batch = d->max_batch;
