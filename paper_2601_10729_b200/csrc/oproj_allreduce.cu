@@ -78,6 +78,7 @@ struct OprojArgs {
   long long kv_block_bytes;
   int part_lo[5];                  // first column of range i (part_lo[parts] = hidden)
   __nv_bfloat16* part_out[4];
+  int rs;                          // split-K reduce-scatter: every CTA of a tile finalises a row slice
 };
 
 // ---------------------------------------------------------------- tcgen05
@@ -115,15 +116,6 @@ __device__ __forceinline__ uint64_t sw128_kmajor_desc(uint32_t saddr) {
 __host__ __device__ constexpr uint32_t umma_idesc_bf16(int m, int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
          (static_cast<uint32_t>(m >> 4) << 24);
-}
-
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                          uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
-      ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
 }
 
 // One 64-element K chunk: four K=16 MMAs (+32 B along the swizzle atom each) in
@@ -367,8 +359,11 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
   //    sums of squares, several lanes per row combined in a fixed shuffle order;
   //  - the residual tile of the first 32 batch rows, staged in smem (16-byte loads).
   __shared__ __align__(16) __nv_bfloat16 res_s[32 * kTileM];
-  const bool res_pre = a.world == 1 && a.residual && split == 0;
-  const bool pro = split == 0 && (kvsel >= 0 || a.ss_in || res_pre);
+  // (with the reduce-scatter every CTA of the tile finalises rows, so every one
+  // needs the per-row inputs; otherwise only the leader)
+  const bool fin = split == 0 || a.rs;
+  const bool res_pre = a.world == 1 && a.residual && fin;
+  const bool pro = fin && (kvsel >= 0 || a.ss_in || res_pre);
   if (pro && warp >= 2) {
     pdl_wait();
     const int pt = threadIdx.x - 64;           // 0..63
@@ -424,6 +419,103 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
   float* red = reinterpret_cast<float*>(smem + static_cast<size_t>(a.stages) * stage_bytes);
   __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(smem);
   if (a.splits > 1) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (a.rs) {
+    // ---- reduce-scatter (world 1, splits in {2, 4, 8}): CTA r of the cluster owns
+    // tile rows [r*128/S, (r+1)*128/S); every row's fp32 partial goes to its owner
+    // (owner's red: [S-1 sources][npad][slice], a warp's rows one contiguous run),
+    // so each CTA takes in (S-1)/S of a tile partial instead of the leader taking
+    // in S-1 of them, and every CTA finalises and stores its own slice.
+    const int S = a.splits, sl = kTileM / S;
+    const int own = m / sl;                       // owner of this thread's row
+    const int my_lo = split * sl;
+    // (tcgen05.ld is warp-wide and .aligned: every lane loads, converged; a warp's
+    // rows can span two owners, so only the stores are predicated)
+    const bool ship = own != split;
+    const int slot_me = split < own ? split : split - 1;
+    const uint32_t dst =
+        ship ? map_to_cta(smem_u32(red + static_cast<size_t>(slot_me) * a.npad * sl + (m - own * sl)), own) : 0u;
+    for (int c = 0; c < a.npad / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld32(trow + c * 32, v);
+      if (ship) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          asm volatile("st.shared::cluster.f32 [%0], %1;"
+                       ::"r"(dst + ((c * 32 + j) * sl) * 4), "f"(__uint_as_float(v[j]))
+                       : "memory");
+      }
+      __syncwarp();
+    }
+    tc_fence_before();
+    cluster_sync_all();                           // every slice's partials have landed
+    tc_fence_after();
+    if (tr) tr[3] = globaltimer();
+    // the owning rows: sources summed in split order (own partial in its place)
+    __nv_bfloat16* stg2 = stg;                    // [npad][sl] bf16 in the (idle) ring
+    if (warp * 32 < my_lo + sl && warp * 32 + 32 > my_lo) {   // warp-uniform
+      const int i = m - my_lo;
+      for (int c = 0; c < a.npad / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(trow + c * 32, v);
+        if (own == split) {
+        // sources in split order, own partial in its place: a compact loop (straight-
+        // line code run once per launch costs instruction fetches, not ALU time)
+        float acc[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+        for (int src = 0; src < S; ++src) {
+          if (src == split) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc[j] += __uint_as_float(v[j]);
+          } else {
+            const float* rp = red + (static_cast<size_t>(src < split ? src : src - 1) * a.npad + c * 32) * sl + i;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc[j] += rp[j * sl];
+          }
+        }
+        if (a.ss_in) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c * 32 + j < a.batch) acc[j] *= rsc[c * 32 + j];
+        }
+        if (a.residual) {
+          const __nv_bfloat16* rb = c == 0 ? res_s + m : a.residual + static_cast<size_t>(c * 32) * a.hidden + tile * kTileM + m;
+          const int rstride = c == 0 ? kTileM : a.hidden;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c * 32 + j < a.batch) acc[j] += __bfloat162float(rb[static_cast<size_t>(j) * rstride]);
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) stg2[(c * 32 + j) * sl + i] = __float2bfloat16_rn(acc[j]);
+        }
+        __syncwarp();
+      }
+    }
+    if (tr) tr[4] = globaltimer();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) tmem_dealloc(tmem, tcols);
+    if (tr) tr[6] = globaltimer();   // the slice stores start
+    // this CTA's slice of the tile: 16-byte vectors per batch row
+    __nv_bfloat16* dst_base = a.out;
+    int dst_stride = a.hidden, col0 = tile * kTileM;
+    for (int r = 0; r < a.parts; ++r)
+      if (col0 >= a.part_lo[r] && col0 < a.part_lo[r + 1]) {
+        dst_base = a.part_out[r];
+        dst_stride = a.part_lo[r + 1] - a.part_lo[r];
+        col0 -= a.part_lo[r];
+      }
+    const int vpr = sl / 8;                       // vectors per batch row
+    for (int q = threadIdx.x; q < a.batch * vpr; q += kThreads) {
+      const int b = q / vpr, o = q - b * vpr;
+      const uint4 val = *reinterpret_cast<const uint4*>(stg2 + b * sl + o * 8);
+      *reinterpret_cast<uint4*>(dst_base + static_cast<size_t>(b) * dst_stride + col0 + my_lo + o * 8) = val;
+      if (kvsel >= 0 && kvoff[b] >= 0)
+        *reinterpret_cast<uint4*>(a.kv_pool + kvoff[b] + (my_lo + o * 8) * 2) = val;
+    }
+    if (tr) tr[5] = globaltimer();
+    return;
+  }
   if (a.splits > 1 && split != 0) {
     // ship this split's fp32 partial into the leader's smem: element (n, m) at
     // n * 128 + m, so a warp's 32 rows are one contiguous 128-byte DSMEM store
@@ -532,18 +624,16 @@ oproj_allreduce_kernel(const __grid_constant__ CUtensorMap wmap,
   if (a.world == 1) {
     // the column range (tensor) this tile belongs to: one lookup per CTA
     __nv_bfloat16* dst_base = a.out;
-    int dst_stride = a.hidden, col0 = tile * kTileM, part = -1;
+    int dst_stride = a.hidden, col0 = tile * kTileM;
     for (int r = 0; r < a.parts; ++r)
       if (col0 >= a.part_lo[r] && col0 < a.part_lo[r + 1]) {
         dst_base = a.part_out[r];
         dst_stride = a.part_lo[r + 1] - a.part_lo[r];
         col0 -= a.part_lo[r];
-        part = r;
       }
     // K3 folded in: a k or v tile is one KV head's 128 dims; its rows also go to
     // the token's slot in the paged pool (resident rows; host-slab rows are the
     // runtime append's, which also fills their staged copy)
-    (void)part;
     for (int i = threadIdx.x; i < nvec; i += kThreads) {
       const int b = i >> 4, o = i & 15;
       *reinterpret_cast<uint4*>(dst_base + static_cast<size_t>(b) * dst_stride + col0 + o * 8) = s4[i];
@@ -944,6 +1034,12 @@ int ofb_oproj_allreduce(const ofb_oproj_desc* d, void* stream) {
   a.kv_max_blocks = d->kv_max_blocks;
   a.kv_part = d->kv_part;
   a.kv_block_bytes = d->kv_block_bytes;
+  {
+    static const int rs_env = std::getenv("OFB_K6_RS") ? std::atoi(std::getenv("OFB_K6_RS")) : 1;
+    // measured (profiles/r02_k6_experiments.md): wins at 8 splits (q/k/v 9.70 -> 8.94 us),
+    // ties at 2, loses at 4 - kept for 8-CTA clusters only
+    a.rs = (rs_env && d->world == 1 && !d->swiglu && !d->ss_out && splits == 8) ? 1 : 0;
+  }
 
 
 

@@ -30,7 +30,7 @@ t = tr.cpu().numpy()
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
 rel = lambda c: (t[:, c][t[:, c] > 0] - t0) / 1e3  # noqa: E731
-names = ["entry", "prologue_done", "acc_ready", "cluster_synced", "output_start", "exit"]
+names = ["entry", "prologue_done", "acc_ready", "cluster_synced", "output_start", "exit", "rs_slice_store"]
 res = {"ctas": int(len(t))}
 for c, n in enumerate(names):
     v = rel(c)
