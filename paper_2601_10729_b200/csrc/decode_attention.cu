@@ -137,6 +137,11 @@ __device__ __forceinline__ void paged_gqa_decode_body(const CUtensorMap& kv_map,
   // launch inputs and this layer's KV may be read - and the producer stream it -
   // while the predecessor drains
   const bool early = a.kv_ready != 0;
+  // kv_ready 3 (= 1 with a late wait): q and this layer's KV are launch inputs,
+  // so the consumers run the whole split before waiting; only the global
+  // writes (partials / out / ticket, which the predecessor's combine may still
+  // read) follow the predecessor's completion
+  const bool late = a.kv_ready == 3;
   if (!early) pdl_wait();
   pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
@@ -213,7 +218,7 @@ __device__ __forceinline__ void paged_gqa_decode_body(const CUtensorMap& kv_map,
     }
   } else {
     // ---------------------------------------------------------- consumers
-    if (early) pdl_wait();
+    if (early && !late) pdl_wait();
     // Q as the A operand (rows = query heads of this group, zero padded).
     uint32_t qa[8][4];
     {
@@ -359,6 +364,7 @@ __device__ __forceinline__ void paged_gqa_decode_body(const CUtensorMap& kv_map,
   __syncthreads();
   merge_weights<kW>(ms, mwt, g, tid);
   __syncthreads();
+  if (late) pdl_wait();
 
   const bool single = (nsplit == 1);
   constexpr int kQ = kHeadDim / 4;
@@ -701,8 +707,11 @@ int attention_cluster_slots(int* slots);
 int attention_cluster_plan(int batch, int hkv, int max_seq_len, const int* slots, int* C, int* P,
                            int* bps, int* stages);
 
-// In-step choice between the split kernel (global ticket + combine) and the
-// cluster kernel (DSMEM combine), from the all-resident step probe
+// Choice between the split kernel (global ticket + combine) and the cluster
+// kernel (DSMEM combine) for launches whose consumers wait for the predecessor
+// first (kv_ready 0 / 2: fetch layers, the whole-decoder step; attention-only
+// in-step launches follow the late-wait policy in launch_decode_attention), from
+// the all-resident step probe before the late wait
 // (tools/small_step_probe.py, profiles/r02_k1_issue_loops.md): the cluster kernel
 // wins with one cluster of <= 4 CTAs per (request, KV head) (8B / 70B at B 4-16,
 // up to 8K) or one cluster with <= 20 blocks per CTA, and with >= 5 clusters per
@@ -803,6 +812,33 @@ static size_t split_workspace_bytes(int batch, int hq, int hkv, int max_seq_len)
   return counters + lse + o;
 }
 
+// Balanced in-step plan: one narrow CTA per SM less one SM per (request, KV
+// head) pair (that pair's combining CTA), so every SM holds one CTA of this
+// layer and the next layer's CTAs fit beside it.  {0, 0} when the split length
+// would exceed the kernel's limits.
+static AttnPlan balanced_plan(int batch, int hkv, int max_seq_len, int num_sms) {
+  AttnPlan p{0, 0};
+  const int nblk = (max_seq_len + kBlockTokens - 1) / kBlockTokens;
+  if (nblk <= 0) return p;
+  const long pairs = (long)batch * hkv;
+  long ns = ((long)num_sms - pairs) / pairs;
+  ns = ns < 1 ? 1 : ns;
+  const int bps = (int)((nblk + ns - 1) / ns);
+  if (bps > kMaxBlocksPerSplit || (nblk + bps - 1) / bps > kMaxSplits) return p;
+  p.blocks_per_split = bps;
+  p.max_splits = (nblk + bps - 1) / bps;
+  return p;
+}
+
+// Where the balanced plan beat the cost-model plan in a step (k1_instep_sweep:
+// 8B and 70B TP8-shard heads, B 1-16, 1K-64K): enough blocks per CTA, or few
+// splits per pair; never with many splits per pair (the combine grows with them).
+static bool balanced_preferred(const AttnPlan& p, int group) {
+  const int ns = p.max_splits, bps = p.blocks_per_split;
+  if (ns > 80) return false;
+  return bps >= 30 || ns <= 8 || (group <= 4 && bps >= 16);
+}
+
 cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void* out,
                                     const int32_t* block_tables, int max_blocks,
                                     const int32_t* seq_lens, void* workspace,
@@ -810,7 +846,35 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
                                     int max_seq_len, float scale, cudaStream_t stream,
                                     int kv_ready, bool standalone) {
   if (batch <= 0) return cudaSuccess;
-  const int variant = pick_variant(batch, hq, hkv, max_seq_len, standalone);
+  // In-step attention-only launches (kv_ready 1: q and KV are launch inputs, the
+  // split kernel's consumers wait for the previous layer only before their global
+  // writes, so consecutive layers overlap): the split kernel, on the balanced
+  // narrow plan (one CTA per SM less one per (request, KV head) pair, so the next
+  // layer's CTAs co-reside) where it measured best, else on the cost-model plan
+  // (tools/k1_instep_sweep.py, profiles/r02_k1_instep.md: with the late wait the
+  // split kernel beat the cluster kernel in a step on every swept shape but one
+  // 1K case).  OFB_K1_INSTEP=split|bal|cluster pins one (tuning only; read at
+  // every launch).
+  int instep = 0;   // 0 auto, 1 split (cost-model plan), 2 balanced narrow, 3 cluster
+  AttnPlan bal{0, 0};
+  if (kv_ready == 1 && hkv > 0 && hq % hkv == 0) {
+    if (const char* f = std::getenv("OFB_K1_INSTEP")) {
+      instep = std::strcmp(f, "split") == 0 ? 1 : std::strcmp(f, "bal") == 0 ? 2
+               : std::strcmp(f, "cluster") == 0 ? 3 : 0;
+    }
+    if (attn_init_once() == cudaSuccess) bal = balanced_plan(batch, hkv, max_seq_len, g_num_sms);
+    if (instep == 0 && k1_variant() == 2)
+      instep = (bal.max_splits > 0 && balanced_preferred(bal, hq / hkv)) ? 2 : 1;
+  }
+  int variant = pick_variant(batch, hq, hkv, max_seq_len, standalone);
+  if (instep == 3) {
+    int slots[5], C, P, bps, stages;
+    if (attention_cluster_slots(slots) == 0 &&
+        attention_cluster_plan(batch, hkv, max_seq_len, slots, &C, &P, &bps, &stages) == 0)
+      variant = 3;
+  } else if (instep == 1 || instep == 2) {
+    variant = 1;
+  }
   if (variant == 3)
     return launch_decode_attention_cluster(map, q, out, block_tables, max_blocks, seq_lens,
                                            workspace, workspace_bytes, batch, hq, hkv,
@@ -825,8 +889,10 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
   if (e != cudaSuccess) return e;
   if (workspace_bytes < split_workspace_bytes(batch, hq, hkv, max_seq_len))
     return cudaErrorInvalidValue;
-  const AttnPlan plan = plan_splits(batch, hq, hkv, max_seq_len, g_num_sms, g_attn_occupancy);
+  AttnPlan plan = plan_splits(batch, hq, hkv, max_seq_len, g_num_sms, g_attn_occupancy);
   const int nblk = (max_seq_len + kBlockTokens - 1) / kBlockTokens;
+  const bool force_narrow = instep == 2 && bal.max_splits > 0;
+  if (force_narrow) plan = bal;
   int ws_splits = nblk < 1 ? 1 : nblk;
   if (ws_splits > kMaxSplits) ws_splits = kMaxSplits;
 
@@ -849,7 +915,8 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
   a.blocks_per_split = plan.blocks_per_split;
   a.max_splits = ws_splits;
   a.scale_log2 = scale * 1.4426950408889634f;
-  a.kv_ready = kv_ready;
+  static const int late_env = std::getenv("OFB_K1_LATE") ? std::atoi(std::getenv("OFB_K1_LATE")) : 1;
+  a.kv_ready = (kv_ready == 1 && late_env) ? 3 : kv_ready;
   a.defer_combine = (variant == 4 && plan.max_splits > 1) ? 1 : 0;
   a.trace = k1_trace_buffer();
   a.trace_ctas = a.trace ? k1_trace_capacity() : 0;
@@ -857,7 +924,7 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
   // one wave at one CTA per SM: the wide instantiation (OFB_K1_WIDE=0|1 pins it)
   const long ctas = (long)plan.max_splits * hkv * batch;
   static const int wide_env = std::getenv("OFB_K1_WIDE") ? std::atoi(std::getenv("OFB_K1_WIDE")) : -1;
-  const bool wide = wide_env >= 0 ? wide_env == 1 : ctas <= g_num_sms;
+  const bool wide = force_narrow ? false : wide_env >= 0 ? wide_env == 1 : ctas <= g_num_sms;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(wide ? (kWideWarps + 1) * 32 : kAttnThreads);
