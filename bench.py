@@ -342,6 +342,27 @@ def reference_control_sample(cfg, decode_tokens: int = 12):
                     "boundary + plan + apply_plan + batch_decode_latency_fast), 1 core"}
 
 
+def host_dram_gbs(threads: int) -> float:
+    """Host DRAM copy bandwidth (SURVEY.md 8(d) CPU baseline item 2): best of 5
+    torch CPU copies of 1 GiB on `threads` threads, read + write bytes / time -
+    the same method as the HBM copy peak."""
+    import torch
+
+    prev = torch.get_num_threads()
+    torch.set_num_threads(threads)
+    try:
+        src = torch.empty(1 << 30, dtype=torch.uint8).fill_(1)
+        dst = torch.empty_like(src)
+        best = float("inf")
+        for _ in range(5):
+            t0 = time.perf_counter()
+            dst.copy_(src)
+            best = min(best, time.perf_counter() - t0)
+        return 2 * src.numel() / best / 1e9
+    finally:
+        torch.set_num_threads(prev)
+
+
 def run_reference_arm(args, cfg):
     """The reference path on this host: kvsim's own control loop (1 core) plus
     the CPU restatement of the data path it prices (oracle port: K3 append + K1
@@ -388,6 +409,8 @@ def run_reference_arm(args, cfg):
     step_ms = data_ms + ctl_ms
     value = cfg["batch"] / (step_ms * 1e-3)
     kv_bytes = int(sum(int(t) for t in sampler.lens)) * cfg["hkv"] * 2 * 128 * 2
+    cpu_gbs = kv_bytes * cfg["layers"] / (data_ms * 1e-3) / 1e9
+    dram_gbs = host_dram_gbs(threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -398,8 +421,10 @@ def run_reference_arm(args, cfg):
                              "timed unscaled"},
         "step_ms": {"data_path_median": data_ms, "control": ctl_ms,
                     "data_path_all": [t * 1e3 for t in times]},
-        "cpu_gbs": kv_bytes * cfg["layers"] / (data_ms * 1e-3) / 1e9,
+        "cpu_gbs": cpu_gbs,
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
+                         "kv_read_gbs": cpu_gbs, "host_dram_copy_gbs": dram_gbs,
+                         "frac_of_host_dram": cpu_gbs / dram_gbs,
                          "sample": f"whole steps: {cfg['layers']} layers x (append + attention "
                                    f"of {cfg['batch']} requests x {cfg['prompt']} tokens), "
                                    "oracle/attn_oracle.c accumulating in f64 over bf16 KV "

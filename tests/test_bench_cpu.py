@@ -22,6 +22,9 @@ def test_reference_arm_prints_contract_line():
         assert key in line
     assert line["value"] > 0 and line["cpu_baseline"]["kind"] == "port"
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+    cb = line["cpu_baseline"]
+    assert cb["host_dram_copy_gbs"] > 0 and cb["kv_read_gbs"] > 0
+    assert abs(cb["frac_of_host_dram"] - cb["kv_read_gbs"] / cb["host_dram_copy_gbs"]) < 1e-9
 
 
 def test_reference_arm_under_torchrun_prints_once():
