@@ -66,6 +66,14 @@ OFB_API int ofb_attention_cluster_slots(int32_t* cluster_slots);
 OFB_API int ofb_attention_split_plan(int32_t batch, int32_t num_q_heads, int32_t num_kv_heads,
                                      int32_t max_seq_len, int32_t num_sms, int32_t ctas_per_sm,
                                      int32_t* blocks_per_split, int32_t* splits);
+/* Host arithmetic: the K1 plan of an attention-only in-step launch (every layer
+ * of a step without fetches but the first) - the split kernel, whose consumers
+ * wait for the previous layer only before their global writes, on the balanced
+ * plan (one narrow CTA per SM less one per (request, KV head) pair; *narrow = 1)
+ * where it measured best, else on the cost-model plan (profiles/r02_k1_instep.md). */
+OFB_API int ofb_attention_instep_plan(int32_t batch, int32_t num_q_heads, int32_t num_kv_heads,
+                                      int32_t max_seq_len, int32_t num_sms, int32_t ctas_per_sm,
+                                      int32_t* blocks_per_split, int32_t* splits, int32_t* narrow);
 /* Diagnostics: stream-K K1 launches write 6 globaltimer stamps per CTA (entry,
  * past the dependency wait, first tile ready, last tile consumed, exit, SM id)
  * into `device_buffer` (uint64 [448][6]); NULL switches tracing off. */

@@ -112,6 +112,9 @@ SIGNATURES = {
     "ofb_attention_cluster_slots": (ctypes.c_int, [ctypes.c_void_p]),
     "ofb_attention_split_plan": (ctypes.c_int, [c_i32, c_i32, c_i32, c_i32, c_i32, c_i32,
                                                 ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)]),
+    "ofb_attention_instep_plan": (ctypes.c_int, [c_i32, c_i32, c_i32, c_i32, c_i32, c_i32,
+                                                 ctypes.POINTER(c_i32), ctypes.POINTER(c_i32),
+                                                 ctypes.POINTER(c_i32)]),
     "ofb_device_info": (ctypes.c_int, [c_i32p, c_i32p]),
     "ofb_host_alloc": (c_vp, [c_i64]),
     "ofb_host_free": (ctypes.c_int, [c_vp]),

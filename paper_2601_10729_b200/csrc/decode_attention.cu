@@ -945,6 +945,29 @@ cudaError_t launch_decode_attention(const CUtensorMap& map, const void* q, void*
   return cudaLaunchKernelEx(&cc, attn_combine_kernel, a);
 }
 
+// Host arithmetic only (no device): the plan an attention-only in-step launch
+// (kv_ready 1) takes under the auto policy - always the split kernel, on the
+// balanced narrow plan where balanced_preferred holds (*narrow = 1), else on the
+// cost-model plan (*narrow = 1 unless that grid is one wave of wide CTAs).
+int attention_instep_plan(int batch, int hq, int hkv, int max_seq_len, int num_sms, int occupancy,
+                          int* blocks_per_split, int* splits, int* narrow) {
+  if (batch < 1 || hkv < 1 || hq % hkv != 0 || hq / hkv > kMaxGroup || max_seq_len < 0 ||
+      num_sms < 1 || occupancy < 1 || !blocks_per_split || !splits || !narrow)
+    return -1;
+  const AttnPlan bal = balanced_plan(batch, hkv, max_seq_len, num_sms);
+  if (bal.max_splits > 0 && balanced_preferred(bal, hq / hkv)) {
+    *blocks_per_split = bal.blocks_per_split;
+    *splits = bal.max_splits;
+    *narrow = 1;
+    return 0;
+  }
+  const AttnPlan p = plan_splits(batch, hq, hkv, max_seq_len, num_sms, occupancy);
+  *blocks_per_split = p.blocks_per_split;
+  *splits = p.max_splits;
+  *narrow = (long)p.max_splits * hkv * batch <= num_sms ? 0 : 1;
+  return 0;
+}
+
 int attention_occupancy() {
   attn_init_once();
   return g_attn_occupancy;

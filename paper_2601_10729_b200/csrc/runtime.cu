@@ -41,6 +41,8 @@ int attention_cluster_plan(int batch, int hkv, int max_seq_len, const int* slots
                            int* bps, int* stages);
 int attention_split_plan(int batch, int hq, int hkv, int max_seq_len, int num_sms, int occupancy,
                          int* blocks_per_split, int* splits);
+int attention_instep_plan(int batch, int hq, int hkv, int max_seq_len, int num_sms, int occupancy,
+                          int* blocks_per_split, int* splits, int* narrow);
 void set_k1_trace_buffer(void* buf, int ctas);
 cudaError_t launch_kv_prefill(const void* k, const void* v, const uint64_t* dst, int num_layers,
                               int tokens, int hkv, cudaStream_t stream);
@@ -380,6 +382,15 @@ int ofb_attention_split_plan(int32_t batch, int32_t num_q_heads, int32_t num_kv_
   if (ofb::attention_split_plan(batch, num_q_heads, num_kv_heads, max_seq_len, num_sms, ctas_per_sm,
                                 blocks_per_split, splits) != 0)
     return ofb::report_error(-1, "ofb_attention_split_plan: bad arguments");
+  return 0;
+}
+
+int ofb_attention_instep_plan(int32_t batch, int32_t num_q_heads, int32_t num_kv_heads,
+                              int32_t max_seq_len, int32_t num_sms, int32_t ctas_per_sm,
+                              int32_t* blocks_per_split, int32_t* splits, int32_t* narrow) {
+  if (ofb::attention_instep_plan(batch, num_q_heads, num_kv_heads, max_seq_len, num_sms, ctas_per_sm,
+                                 blocks_per_split, splits, narrow) != 0)
+    return ofb::report_error(-1, "ofb_attention_instep_plan: bad arguments");
   return 0;
 }
 

@@ -176,3 +176,53 @@ def test_k1_split_plan_invariants():
     assert _split_plan(lib, 16, 32, 8, 32768) == (256, 8)    # the cfg2 layer: 1024 CTAs
     bad = ctypes.c_int32()
     assert lib.ofb_attention_split_plan(1, 6, 4, 100, 148, 2, ctypes.byref(bad), ctypes.byref(bad)) != 0
+
+
+def _instep_plan(lib, b, hq, hkv, seq, sms=148, occ=3):
+    import ctypes
+
+    bps, ns, narrow = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    assert lib.ofb_attention_instep_plan(b, hq, hkv, seq, sms, occ, ctypes.byref(bps),
+                                         ctypes.byref(ns), ctypes.byref(narrow)) == 0
+    return bps.value, ns.value, narrow.value
+
+
+def test_k1_instep_plan_follows_the_sweep():
+    """The attention-only in-step K1 plan takes the balanced narrow grid exactly where
+    tools/k1_instep_sweep.py measured it > 5 % faster than the cost-model plan, and the
+    cost-model plan where that was > 5 % faster (profiles/r02_k1_instep_sweep.jsonl;
+    the sequence length in a step is the context + 1)."""
+    from paper_2601_10729_b200 import _native
+
+    lib = _native.load()
+    heads = {"8B": (32, 8), "70B-TP8-shard": (8, 1)}
+    bal_wins = [("8B", 1, 4096), ("8B", 1, 8192), ("8B", 1, 16384), ("8B", 2, 1024),
+                ("8B", 2, 4096), ("8B", 2, 8192), ("8B", 4, 1024), ("8B", 4, 4096),
+                ("8B", 8, 1024), ("8B", 16, 1024), ("70B-TP8-shard", 2, 65536),
+                ("70B-TP8-shard", 4, 32768), ("70B-TP8-shard", 4, 65536),
+                ("70B-TP8-shard", 8, 8192), ("70B-TP8-shard", 8, 16384),
+                ("70B-TP8-shard", 8, 32768), ("70B-TP8-shard", 16, 4096),
+                ("70B-TP8-shard", 16, 8192), ("70B-TP8-shard", 16, 16384)]
+    split_wins = ([("70B-TP8-shard", 1, c) for c in (1024, 4096, 8192, 16384, 32768, 65536)]
+                  + [("70B-TP8-shard", 2, c) for c in (1024, 4096, 8192, 16384, 32768)]
+                  + [("70B-TP8-shard", 4, c) for c in (1024, 4096, 8192, 16384)]
+                  + [("70B-TP8-shard", 8, 1024), ("70B-TP8-shard", 8, 4096)])
+    for name, b, ctx in bal_wins + split_wins:
+        hq, hkv = heads[name]
+        bps, ns, narrow = _instep_plan(lib, b, hq, hkv, ctx + 1)
+        nblk = -(-(ctx + 1) // 16)
+        nominal = max(1, (148 - b * hkv) // (b * hkv))    # one narrow CTA per SM less one per pair
+        balanced = narrow == 1 and bps == -(-nblk // nominal) and ns == -(-nblk // bps)
+        assert balanced == ((name, b, ctx) in bal_wins), (name, b, ctx, bps, ns, narrow)
+        assert ns * bps >= nblk and bps <= 256 and ns <= 256
+
+
+def test_k1_instep_plan_rejects_bad_shapes():
+    import ctypes
+
+    from paper_2601_10729_b200 import _native
+
+    lib = _native.load()
+    bad = ctypes.c_int32()
+    assert lib.ofb_attention_instep_plan(1, 6, 4, 100, 148, 3, ctypes.byref(bad), ctypes.byref(bad),
+                                         ctypes.byref(bad)) != 0
