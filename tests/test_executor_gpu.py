@@ -451,3 +451,39 @@ def test_full_step_other_head_layouts(hq, hkv):
                 r.record_generated_token()
     finally:
         ex.close()
+
+
+@pytest.mark.parametrize("mode", ["auto", "bal", "split"])
+@pytest.mark.parametrize("heads,B,ctx", [((32, 8), 1, 4096), ((32, 8), 2, 1500), ((8, 1), 3, 2900),
+                                         ((32, 8), 4, 1024)])
+def test_attention_only_steps_late_wait_and_balanced_plan(monkeypatch, heads, B, ctx, mode):
+    """All-resident steps (every layer but the first launched kv_ready: K1's consumers
+    wait for the previous layer only before their global writes) on the balanced narrow
+    plan, the cost-model plan and the auto policy: every layer of several consecutive
+    steps equals the oracle (profiles/r02_k1_instep.md)."""
+    from paper_2601_10729_b200 import _native
+    from paper_2601_10729_b200.executor import ModelShape
+
+    if mode == "auto":
+        monkeypatch.delenv("OFB_K1_INSTEP", raising=False)
+    else:
+        monkeypatch.setenv("OFB_K1_INSTEP", mode)
+    hq, hkv = heads
+    shape = ModelShape(4, hq, hkv)
+    batch = [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=ctx - 53 * i, target_output_tokens=16)
+             for i in range(B)]
+    cap = -(-(ctx + 20) // 16)
+    ex = _executor(shape, device_blocks=B * 4 * cap + 16, host_blocks=16)
+    ex.install(batch, PlacementMatrix.from_strides(range(B), 4, [None] * B))
+    if mode == "bal" and B == 1 and hkv == 8:   # the plan this case exists for
+        import ctypes
+        bps, ns, narrow = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        assert _native.load().ofb_attention_instep_plan(B, hq, hkv, ctx + 1, 148, 3, ctypes.byref(bps),
+                                                        ctypes.byref(ns), ctypes.byref(narrow)) == 0
+        assert narrow.value == 1 and ns.value * hkv * B <= 148
+    for _ in range(3):
+        ex.decode_step(batch, None, None, sync=True)
+        _check_step_outputs(ex, batch)
+        for r in batch:
+            r.record_generated_token()
+    ex.close()

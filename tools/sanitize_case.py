@@ -101,4 +101,21 @@ for _ in range(2):
 torch.cuda.synchronize()
 dec.close()
 ex.close()
+
+# attention-only all-resident steps: K1's consumers wait after the math (kv_ready 1),
+# on the balanced narrow plan (8 KV heads, B=1, 4K: 17 splits x 8 pairs) and on the
+# cost-model plan (1 KV head, B=2)
+for (hq, hkv), B, ctx in (((32, 8), 1, 4096), ((8, 1), 2, 3000)):
+    shape = ModelShape(3, hq, hkv)
+    cap = -(-(ctx + 8) // 16)
+    batch = [RequestState(id=i, arrival_time_ms=0.0, prompt_tokens=ctx - 37 * i, target_output_tokens=8)
+             for i in range(B)]
+    ex = B200Executor(shape, device_blocks=B * 3 * cap + 16, host_blocks=16)
+    ex.install(batch, PlacementMatrix.from_strides(range(B), 3, [None] * B))
+    inp = ex.synthetic_inputs(B, step=0)
+    for _ in range(3):
+        ex.decode_step(batch, None, inp, sync=False)
+    ex.drain()
+    torch.cuda.synchronize()
+    ex.close()
 print("sanitize case done")
