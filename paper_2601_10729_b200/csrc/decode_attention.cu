@@ -34,7 +34,7 @@ constexpr int kStages = 8;
 constexpr int kWideWarps = 8;
 constexpr int kWideStages = 24;
 constexpr int kMaxSplits = 256;
-constexpr int kMaxBlocksPerSplit = 256;
+constexpr int kMaxBlocksPerSplit = 512;   // the balanced in-step plan goes past the cost model's 256
 // Split tickets live in a fixed region at the start of the workspace, sized for
 // the largest (request x kv head) grid, so partials of a previous launch with
 // a different batch can never alias a counter.

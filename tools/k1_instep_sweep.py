@@ -30,6 +30,8 @@ def _arg(flag, default):
 MODES = os.environ.get("SWEEP_MODES", "auto,split,bal,cluster").split(",")
 max_tokens = _arg("--max-tokens", [262144])[0]
 shapes = {"8B": ModelShape(32, 32, 8), "70B-TP8-shard": ModelShape(32, 8, 1)}
+if os.environ.get("SWEEP_SHAPES"):
+    shapes = {k: v for k, v in shapes.items() if k in os.environ["SWEEP_SHAPES"].split(",")}
 for name, shape in shapes.items():
     for B in _arg("--batches", (1, 2, 4, 8, 16)):
         for ctx in _arg("--contexts", (1024, 4096, 8192, 16384, 32768, 65536)):
