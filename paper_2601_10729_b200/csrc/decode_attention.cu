@@ -34,7 +34,14 @@ constexpr int kStages = 8;
 constexpr int kWideWarps = 8;
 constexpr int kWideStages = 24;
 constexpr int kMaxSplits = 256;
-constexpr int kMaxBlocksPerSplit = 512;   // the balanced in-step plan goes past the cost model's 256
+constexpr int kMaxBlocksPerSplit = 256;         // cost-model plans (both instantiations)
+// the narrow instantiation's block-table run holds 512 entries so the balanced
+// in-step plan (narrow only) reaches past 256 blocks per split; the wide one
+// stays at 256: one more KiB would push its smem past the 196 KB carve-out and
+// halve L1 (latency-bound launches measured 0.3-0.45 us slower)
+constexpr int kMaxBlocksPerSplitNarrow = 512;
+template <int kW>
+constexpr int blk_cap() { return kW == kWideWarps ? kMaxBlocksPerSplit : kMaxBlocksPerSplitNarrow; }
 // Split tickets live in a fixed region at the start of the workspace, sized for
 // the largest (request x kv head) grid, so partials of a previous launch with
 // a different batch can never alias a counter.
@@ -84,12 +91,12 @@ static_assert(sizeof(MergeSlots<kWideWarps>) + sizeof(MergeWeights<kWideWarps>) 
 template <int kW, int kS>
 constexpr size_t attn_smem_bytes() {
   return 1024 + size_t(kS) * kHeadBlockBytes + 2 * kS * sizeof(uint64_t) +
-         kMaxBlocksPerSplit * sizeof(int32_t) + 16;
+         blk_cap<kW>() * sizeof(int32_t) + 16;
 }
 
 constexpr size_t kAttnSmemBytes = 1024 /*align slack*/ + kRingBytes +
                                   2 * kStages * sizeof(uint64_t) +
-                                  kMaxBlocksPerSplit * sizeof(int32_t) + 16;
+                                  kMaxBlocksPerSplitNarrow * sizeof(int32_t) + 16;
 
 // acc += sum_u w[s + u*parts] * src[(s + u*parts) rows]: N float4 partial loads
 // in flight, then the FMAs in split order.
@@ -151,7 +158,7 @@ __device__ __forceinline__ void paged_gqa_decode_body(const CUtensorMap& kv_map,
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + kRing);
   uint64_t* empty = full + kS;
   int32_t* blk_ids = reinterpret_cast<int32_t*>(empty + kS);
-  int* flag = blk_ids + kMaxBlocksPerSplit;
+  int* flag = blk_ids + blk_cap<kW>();
   // The split's table run is loaded speculatively (bounded by the row, not by
   // the sequence length) so it does not wait for the seq_lens round trip.
   const int b_begin = split * a.blocks_per_split;
@@ -824,7 +831,7 @@ static AttnPlan balanced_plan(int batch, int hkv, int max_seq_len, int num_sms) 
   long ns = ((long)num_sms - pairs) / pairs;
   ns = ns < 1 ? 1 : ns;
   const int bps = (int)((nblk + ns - 1) / ns);
-  if (bps > kMaxBlocksPerSplit || (nblk + bps - 1) / bps > kMaxSplits) return p;
+  if (bps > kMaxBlocksPerSplitNarrow || (nblk + bps - 1) / bps > kMaxSplits) return p;
   p.blocks_per_split = bps;
   p.max_splits = (nblk + bps - 1) / bps;
   return p;
